@@ -1,0 +1,95 @@
+/*
+ * flashfps_b200.h — C ABI of the B200-native FlashFPS hot path.
+ *
+ * The reference (arxiv/paper_2604_17720, pkg/src/flashfps) has no FFI: its
+ * hot path is the Python function
+ *
+ *     run_kernel(points (n,3) f64, m, seed_pos, threads=1)
+ *         -> (order int64[m], selection_dist2 f64[m], distance_evals)
+ *                                        pkg/src/flashfps/fps_core.py:110-175
+ *
+ * called from fps (fps_core.py:193), fps_prune (fps_prune.py:92),
+ * verify_prefix_property (fps_cache.py:177) and run_restricted
+ * (fps_cache.py:196).  Each entry point below replaces one of those seams
+ * for a whole batch of clouds; the Python mirror of the reference API
+ * (paper_2604_17720_b200/) binds them through ctypes (GIL released during the
+ * call).  INTEGRATION.md shows the binding.
+ *
+ * Conventions
+ *   - All data pointers are DEVICE pointers (cudaMalloc / torch CUDA tensors)
+ *     on the current device, except where a name ends in _host.
+ *   - `stream` is a cudaStream_t (NULL = legacy default stream).  Calls are
+ *     stream-ordered and do not synchronize the host, except *_host.
+ *   - Return value: FFPS_OK (0) or a negative FFPS_E* code; the message of
+ *     the last failure on the calling thread is ffps_last_error().
+ *   - No global mutable state besides per-device kernel attribute caches;
+ *     calls on different streams / host threads are independent.
+ *   - Argument validation mirrors the reference's exceptions, which the
+ *     Python layer raises BEFORE calling in (fps_core.py:178-182,
+ *     fps_prune.py:78-88): a violated precondition here returns FFPS_EINVAL.
+ */
+#ifndef FLASHFPS_B200_H
+#define FLASHFPS_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FFPS_ABI_VERSION 1
+
+enum ffps_dtype { FFPS_F32 = 0, FFPS_F64 = 1 };
+
+enum ffps_status {
+  FFPS_OK = 0,
+  FFPS_EINVAL = -1,       /* precondition violated (budget, seed, sizes)   */
+  FFPS_EUNSUPPORTED = -2, /* shape outside every kernel configuration       */
+  FFPS_ECUDA = -3         /* CUDA runtime / launch failure                 */
+};
+
+/* Farthest-first selection over a batch of clouds (replaces run_kernel,
+ * fps_core.py:110-175, and its run_restricted form, fps_cache.py:189-201).
+ *
+ *   xyz          [batch][cloud_stride][3] AoS, float or double (dtype)
+ *   n            points per cloud taking part: the candidate prefix
+ *                xyz[b][0:n) (candidate pruning is a prefix slice,
+ *                fps_prune.py:54-65,92) — or, when index_map != NULL, the
+ *                gathered points xyz[b][index_map[b][i]], i < n
+ *   iters        greedy iterations m (or the pruned budget k), 1 <= iters <= n
+ *   seed_pos     [batch] int64 start positions (local to the point set)
+ *   index_map    NULL or [batch][map_stride] int64 original indices
+ *   order        [batch][out_stride] int64: order[b][0:iters) receives the
+ *                selected ORIGINAL indices (mapped through index_map)
+ *   sel_d2       [batch][out_stride] float/double: selection distances,
+ *                sel_d2[b][0] = +inf
+ * Ties break to the lowest position; results are bit-identical to the
+ * reference's binary64 (F64) or to the same algorithm in binary32 (F32). */
+int ffps_run_kernel(int dtype, const void* xyz, int64_t batch,
+                    int64_t cloud_stride, int64_t n, int64_t iters,
+                    const int64_t* seed_pos, const int64_t* index_map,
+                    int64_t map_stride, int64_t* order, void* sel_d2,
+                    int64_t out_stride, void* stream);
+
+/* Budget fill, FillMode.DETERMINISTIC_SLICE (fps_prune.py:96-100,104-105):
+ * for every cloud writes order[b][k + w], w < m1 - k, = the w-th smallest
+ * index of [0, n) absent from order[b][0:k), and sel_d2[b][k + w] = 0. */
+int ffps_fill_slice(int dtype, int64_t* order, void* sel_d2, int64_t batch,
+                    int64_t out_stride, int64_t k, int64_t m1, void* stream);
+
+/* Kernel configuration the library would use (for benches / reports).
+ * out[0]=threads/CTA, out[1]=register slots/thread, out[2]=smem slots/thread,
+ * out[3]=spill slots/thread, out[4]=CTAs per cluster (per cloud),
+ * out[5]=resident CTAs per SM, out[6]=max resident clusters on the device. */
+int ffps_plan(int dtype, int64_t n, int64_t batch, int64_t* out);
+
+/* Number of kernel launches the last successful call on this thread issued. */
+int64_t ffps_last_launch_count(void);
+
+const char* ffps_last_error(void);
+int ffps_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FLASHFPS_B200_H */

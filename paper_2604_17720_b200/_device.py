@@ -1,0 +1,87 @@
+"""Device plumbing between torch tensors and the C ABI.
+
+torch provides device memory, pinned host memory and streams; every FLOP of
+the hot path runs in the library's own kernels (K1 greedy, K2 fill).  The
+launch counter lets benches report how many of those kernels ran.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _native
+from .errors import KernelError
+
+_DTYPE_CODE = {torch.float32: _native.F32, torch.float64: _native.F64}
+_launches = 0
+
+
+def launches() -> int:
+    """Kernel launches issued by this process so far (K1 + K2)."""
+    return _launches
+
+
+def _count(n: int) -> None:
+    global _launches
+    _launches += n
+
+
+def require_cuda(device=None) -> torch.device:
+    if not torch.cuda.is_available():
+        raise KernelError("no CUDA device is available; the FlashFPS path has no CPU fallback")
+    _native.load()
+    dev = torch.device("cuda", torch.cuda.current_device()) if device is None \
+        else torch.device(device)
+    if dev.type != "cuda":
+        raise KernelError(f"device {dev} is not a CUDA device")
+    return dev
+
+
+def dtype_code(t: torch.Tensor) -> int:
+    try:
+        return _DTYPE_CODE[t.dtype]
+    except KeyError:
+        raise TypeError(f"coordinates must be float32 or float64, got {t.dtype}") from None
+
+
+def _stream_handle(stream) -> int:
+    s = torch.cuda.current_stream() if stream is None else stream
+    return int(s.cuda_stream)
+
+
+def greedy(xyz: torch.Tensor, n: int, iters: int, seeds: torch.Tensor,
+           order: torch.Tensor, sel: torch.Tensor, index_map: torch.Tensor | None = None,
+           stream=None) -> None:
+    """K1 over a batch: xyz (B, N, 3) CUDA, contiguous; writes order[:, :iters]
+    and sel[:, :iters] (row stride = order.stride(0))."""
+    B = xyz.shape[0]
+    if B == 0:
+        return
+    assert xyz.is_cuda and xyz.is_contiguous() and xyz.dim() == 3 and xyz.shape[2] == 3
+    assert order.dtype == torch.int64 and order.stride(1) == 1 and sel.stride(1) == 1
+    assert sel.dtype == xyz.dtype and sel.stride(0) == order.stride(0)
+    assert seeds.dtype == torch.int64 and seeds.is_cuda and seeds.numel() == B
+    map_ptr, map_stride = None, 0
+    if index_map is not None:
+        assert index_map.dtype == torch.int64 and index_map.stride(1) == 1
+        map_ptr, map_stride = index_map.data_ptr(), index_map.stride(0)
+    with torch.cuda.device(xyz.device):
+        _count(_native.run_kernel(dtype_code(xyz), xyz.data_ptr(), B, xyz.shape[1], n, iters,
+                                  seeds.data_ptr(), map_ptr, map_stride, order.data_ptr(),
+                                  sel.data_ptr(), order.stride(0), _stream_handle(stream)))
+
+
+def fill_slice(order: torch.Tensor, sel: torch.Tensor, k: int, m1: int, stream=None) -> None:
+    """K2: order[:, k:m1] <- first ascending unselected indices, sel[:, k:m1] <- 0."""
+    B = order.shape[0]
+    if B == 0 or m1 <= k:
+        return
+    with torch.cuda.device(order.device):
+        _count(_native.fill_slice(dtype_code(sel), order.data_ptr(), sel.data_ptr(), B,
+                                  order.stride(0), k, m1, _stream_handle(stream)))
+
+
+def seeds_tensor(seed_index, B: int, device) -> torch.Tensor:
+    arr = np.broadcast_to(np.asarray(seed_index, dtype=np.int64), (B,))
+    return torch.from_numpy(np.ascontiguousarray(arr)).to(device, non_blocking=False)

@@ -1,0 +1,90 @@
+"""ctypes binding of the C ABI in include/flashfps_b200.h.
+
+The library (``_lib/libflashfps_b200.so``, built in-tree by
+``__graft_entry__.build()`` / ``make -C paper_2604_17720_b200/csrc``) is the
+only compute path: if it is missing, or no CUDA device is usable, every call
+raises KernelError — there is no CPU fallback.  ctypes.CDLL releases the GIL
+for the duration of each foreign call.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+from .errors import KernelError
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib",
+                        "libflashfps_b200.so")
+
+F32, F64 = 0, 1
+_STATUS = {-1: "EINVAL", -2: "EUNSUPPORTED", -3: "ECUDA"}
+
+_lock = threading.Lock()
+_lib = None
+
+# (symbol, restype, argtypes) — must match include/flashfps_b200.h
+_i64, _vp, _int = ctypes.c_int64, ctypes.c_void_p, ctypes.c_int
+SIGNATURES = {
+    "ffps_run_kernel": (_int, [_int, _vp, _i64, _i64, _i64, _i64, _vp, _vp, _i64, _vp,
+                               _vp, _i64, _vp]),
+    "ffps_fill_slice": (_int, [_int, _vp, _vp, _i64, _i64, _i64, _i64, _vp]),
+    "ffps_plan": (_int, [_int, _i64, _i64, ctypes.POINTER(_i64)]),
+    "ffps_last_launch_count": (_i64, []),
+    "ffps_last_error": (ctypes.c_char_p, []),
+    "ffps_abi_version": (_int, []),
+}
+
+
+def load():
+    """Load (once) and return the ctypes library; raises KernelError."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                raise KernelError(
+                    f"CUDA library not built: {LIB_PATH} is missing "
+                    "(run __graft_entry__.build() or make -C paper_2604_17720_b200/csrc)")
+            lib = ctypes.CDLL(LIB_PATH)
+            for name, (res, args) in SIGNATURES.items():
+                fn = getattr(lib, name)
+                fn.restype = res
+                fn.argtypes = args
+            if lib.ffps_abi_version() != 1:
+                raise KernelError("ABI version mismatch")
+            _lib = lib
+    return _lib
+
+
+def check(rc: int, what: str) -> None:
+    if rc != 0:
+        msg = load().ffps_last_error().decode(errors="replace")
+        raise KernelError(f"{what} failed ({_STATUS.get(rc, rc)}): {msg}")
+
+
+def run_kernel(dtype, xyz, batch, cloud_stride, n, iters, seed_pos, index_map, map_stride,
+               order, sel_d2, out_stride, stream) -> int:
+    lib = load()
+    check(lib.ffps_run_kernel(dtype, xyz, batch, cloud_stride, n, iters, seed_pos,
+                              index_map, map_stride, order, sel_d2, out_stride, stream),
+          "ffps_run_kernel")
+    return int(lib.ffps_last_launch_count())
+
+
+def fill_slice(dtype, order, sel_d2, batch, out_stride, k, m1, stream) -> int:
+    lib = load()
+    check(lib.ffps_fill_slice(dtype, order, sel_d2, batch, out_stride, k, m1, stream),
+          "ffps_fill_slice")
+    return int(lib.ffps_last_launch_count())
+
+
+def plan(dtype: int, n: int, batch: int) -> dict:
+    lib = load()
+    out = (ctypes.c_int64 * 7)()
+    check(lib.ffps_plan(dtype, n, batch, out), "ffps_plan")
+    keys = ("threads", "reg_slots", "smem_slots", "spill_slots", "cluster",
+            "ctas_per_sm", "max_clusters")
+    return dict(zip(keys, (int(v) for v in out)))

@@ -1,0 +1,283 @@
+"""Batched device API: the whole hot path for B clouds per call.
+
+Every function takes a batch of clouds ``xyz`` of shape (B, N, 3) — a CUDA
+tensor (float32 or float64), or a host array/tensor that is copied to the
+current device — and keeps all intermediate results on the device:
+
+* ``fps_batch``               fps            (fps_core.py:185-196)
+* ``fps_prune_batch``         fps_prune      (fps_prune.py:68-111)
+* ``run_restricted_batch``    run_restricted (fps_cache.py:189-201)
+* ``hierarchical_sample_batch`` hierarchical_sample_detailed (fps_cache.py:204-240)
+* ``hierarchical_sample_host``  the same from/to host buffers (the end-to-end
+  call the benchmark times: H2D copy, kernels, D2H copy)
+
+Validation raises the reference's exceptions before any device work; the
+stats are the reference's analytic counters for ONE cloud (every cloud of a
+batch has the same shape, so the same counters).  The single-cloud API in
+fps_core / fps_prune / fps_cache is this module with B = 1.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Sequence
+
+import numpy as np
+import torch
+
+from . import _device
+from .errors import (BudgetExceedsCloud, BudgetOutOfRange, SeedNotInCandidates,
+                     SeedOutOfRange)
+from .fps_core import OrderedSample, SamplerStats
+from .fps_prune import FillMode, PruneConfig
+
+__all__ = ["BatchSample", "as_device_batch", "fps_batch", "fps_prune_batch",
+           "run_restricted_batch", "hierarchical_sample_batch", "hierarchical_sample_host",
+           "cache_footprint_bytes"]
+
+BYTES_PER_ENTRY = 36  # fps_cache.py:28 (uint32 index + 3 x f64 + f64 dist2)
+
+
+@dataclass
+class BatchSample:
+    """Ordered samples of B clouds: ``indices`` (B, M) int64 original
+    indices and ``selection_dist2`` (B, M) in the input dtype, on the device.
+    Cache-on deeper layers are views (prefix slices) of layer 1."""
+
+    indices: torch.Tensor
+    selection_dist2: torch.Tensor
+    fill_boundary: int
+
+    def __len__(self) -> int:
+        return int(self.indices.shape[1])
+
+    def to_ordered(self, b: int) -> OrderedSample:
+        return OrderedSample(self.indices[b].cpu().numpy(),
+                             self.selection_dist2[b].to(torch.float64).cpu().numpy(),
+                             fill_boundary=self.fill_boundary)
+
+
+def cache_footprint_bytes(m1: int) -> int:
+    if m1 < 1:
+        raise BudgetOutOfRange(f"cache size must be >= 1; got {m1}")
+    return int(m1) * BYTES_PER_ENTRY
+
+
+def as_device_batch(xyz, device=None) -> torch.Tensor:
+    """(B, N, 3) contiguous CUDA float32/float64 tensor (a (N, 3) input is a
+    batch of one).  Host inputs are copied; float64 stays float64."""
+    dev = _device.require_cuda(device)
+    if isinstance(xyz, torch.Tensor):
+        t = xyz
+    else:
+        a = np.asarray(xyz)
+        if a.dtype not in (np.float32, np.float64):
+            a = a.astype(np.float64)
+        t = torch.from_numpy(a if a.flags.writeable and a.flags.c_contiguous
+                             else np.array(a, order="C"))
+    if t.dtype not in (torch.float32, torch.float64):
+        t = t.to(torch.float64)
+    if t.dim() == 2:
+        t = t.unsqueeze(0)
+    if t.dim() != 3 or t.shape[2] != 3:
+        raise ValueError(f"points must have shape (B, N, 3); got {tuple(t.shape)}")
+    if t.shape[1] < 1:
+        raise BudgetOutOfRange("cloud is empty")
+    if t.device != dev:
+        t = t.to(dev, non_blocking=t.is_pinned())
+    return t.contiguous()
+
+
+def _shape(xyz) -> tuple[int, int]:
+    """(B, N) of a (B, N, 3) or (N, 3) input without touching the device, so
+    argument errors surface before any CUDA requirement."""
+    shp = tuple(xyz.shape) if hasattr(xyz, "shape") else np.shape(xyz)
+    if len(shp) == 2:
+        shp = (1,) + shp
+    if len(shp) != 3 or shp[2] != 3:
+        raise ValueError(f"points must have shape (B, N, 3); got {shp}")
+    return int(shp[0]), int(shp[1])
+
+
+def _seed_array(seed_index, B: int) -> np.ndarray:
+    return np.broadcast_to(np.asarray(seed_index, dtype=np.int64), (B,))
+
+
+def _check_seeds(seeds: np.ndarray, n: int) -> None:
+    bad = (seeds < 0) | (seeds >= n)
+    if bad.any():
+        s = int(seeds[np.flatnonzero(bad)[0]])
+        raise SeedOutOfRange(f"seed index {s} not in [0, {n})")
+
+
+def fps_batch(xyz, m: int, seed_index=0, *, device=None) -> tuple[BatchSample, SamplerStats]:
+    """Exhaustive FPS of every cloud (fps_core.py:185-196)."""
+    B, n = _shape(xyz)
+    if not 1 <= m <= n:
+        raise BudgetOutOfRange(f"m={m} not in [1, {n}]")
+    seeds = _seed_array(seed_index, B)
+    _check_seeds(seeds, n)
+    x = as_device_batch(xyz, device)
+    order = torch.empty((B, m), dtype=torch.int64, device=x.device)
+    sel = torch.empty((B, m), dtype=x.dtype, device=x.device)
+    _device.greedy(x, n, m, _device.seeds_tensor(seeds, B, x.device), order, sel)
+    return (BatchSample(order, sel, m),
+            SamplerStats(distance_evals=n * (m - 1), iterations=m, candidates=n))
+
+
+def _random_fill(order: torch.Tensor, sel: torch.Tensor, k: int, m1: int, n: int,
+                 rng_seed: int) -> None:
+    """FillMode.SEEDED_RANDOM (fps_prune.py:101-103) — NumPy's Generator.choice
+    on the host, same call as the reference; off the default path."""
+    picks = order[:, :k].cpu().numpy()
+    fills = np.empty((picks.shape[0], m1 - k), dtype=np.int64)
+    for b in range(picks.shape[0]):
+        remaining = np.ones(n, dtype=bool)
+        remaining[picks[b]] = False
+        pool = np.flatnonzero(remaining)
+        fills[b] = np.random.default_rng(rng_seed).choice(pool, size=m1 - k, replace=False)
+    order[:, k:m1].copy_(torch.from_numpy(fills))
+    sel[:, k:m1].zero_()
+
+
+def _fps_prune_checks(B: int, n: int, m1: int, cfg: PruneConfig, seeds: np.ndarray):
+    """fps_prune.py:78-88 — returns (k, c)."""
+    if not 1 <= m1 <= n:
+        raise BudgetOutOfRange(f"m1={m1} not in [1, {n}]")
+    _check_seeds(seeds, n)
+    k = cfg.kernel_budget(m1)
+    c = min(cfg.candidate_count(n, m1), n)   # candidate_prune(...).shape[0]
+    if (seeds >= c).any():
+        s = int(seeds[np.flatnonzero(seeds >= c)[0]])
+        raise SeedNotInCandidates(
+            f"seed index {s} was pruned (candidate count {c}); "
+            "re-index the cloud or lower p")
+    return k, c
+
+
+def _fps_prune_device(x: torch.Tensor, m1: int, cfg: PruneConfig, seeds: np.ndarray):
+    B, n = x.shape[0], x.shape[1]
+    k, c = _fps_prune_checks(B, n, m1, cfg, seeds)
+    order = torch.empty((B, m1), dtype=torch.int64, device=x.device)
+    sel = torch.empty((B, m1), dtype=x.dtype, device=x.device)
+    # candidates are the store prefix [0, c): kernel positions == original indices
+    _device.greedy(x, c, k, _device.seeds_tensor(seeds, B, x.device), order, sel)
+    if m1 > k:
+        if cfg.fill_mode is FillMode.DETERMINISTIC_SLICE:
+            _device.fill_slice(order, sel, k, m1)
+        else:
+            _random_fill(order, sel, k, m1, n, cfg.rng_seed)
+    return (BatchSample(order, sel, k),
+            SamplerStats(distance_evals=c * (k - 1), iterations=k, candidates=c))
+
+
+def fps_prune_batch(xyz, m1: int, cfg: PruneConfig, seed_index=0, *,
+                    device=None) -> tuple[BatchSample, SamplerStats]:
+    """FPS-Prune for every cloud (fps_prune.py:68-111)."""
+    B, n = _shape(xyz)
+    seeds = _seed_array(seed_index, B)
+    _fps_prune_checks(B, n, m1, cfg, seeds)
+    return _fps_prune_device(as_device_batch(xyz, device), m1, cfg, seeds)
+
+
+def run_restricted_batch(xyz, index_map, m: int, seed_pos=0, *,
+                         device=None) -> tuple[BatchSample, SamplerStats]:
+    """Exact FPS over xyz[b][index_map[b]] in map order, reported in original
+    indices (fps_cache.py:189-201); the gather happens inside the kernel."""
+    B, _ = _shape(xyz)
+    nm = int(np.shape(index_map)[-1])
+    if not 1 <= m <= nm:
+        raise BudgetOutOfRange(f"m={m} not in [1, {nm}]")
+    seeds = _seed_array(seed_pos, B)
+    _check_seeds(seeds, nm)
+    x = as_device_batch(xyz, device)
+    imap = index_map if isinstance(index_map, torch.Tensor) else \
+        torch.from_numpy(np.ascontiguousarray(np.asarray(index_map, dtype=np.int64)))
+    if imap.dim() == 1:
+        imap = imap.unsqueeze(0)
+    imap = imap.to(x.device, torch.int64)
+    if imap.stride(-1) != 1:
+        imap = imap.contiguous()
+    order = torch.empty((B, m), dtype=torch.int64, device=x.device)
+    sel = torch.empty((B, m), dtype=x.dtype, device=x.device)
+    _device.greedy(x, nm, m, _device.seeds_tensor(seeds, B, x.device), order, sel,
+                   index_map=imap)
+    return (BatchSample(order, sel, m),
+            SamplerStats(distance_evals=nm * (m - 1), iterations=m, candidates=nm))
+
+
+def _budgets(budgets) -> tuple[int, ...]:
+    from .fps_cache import LayerBudgets
+    if not isinstance(budgets, LayerBudgets):
+        budgets = LayerBudgets(tuple(budgets))
+    return budgets.budgets
+
+
+def hierarchical_sample_batch(xyz, budgets: Sequence[int], cfg: PruneConfig, seed_index=0,
+                              cache_enabled: bool = True, *, device=None):
+    """Every layer of the budget pyramid for every cloud
+    (fps_cache.py:204-240).  Returns (layers, total, per_layer): with the cache
+    on, layers 2..L are prefix views of layer 1 (zero distance evaluations);
+    with it off, each layer re-runs exact FPS on the previous layer's points,
+    seeded at position 0 (the reference's verification / exhaustive path)."""
+    b = _budgets(budgets)
+    B, n = _shape(xyz)
+    if b[0] > n:
+        raise BudgetExceedsCloud(f"M1={b[0]} exceeds cloud size {n}")
+    seeds = _seed_array(seed_index, B)
+    _fps_prune_checks(B, n, b[0], cfg, seeds)
+    x = as_device_batch(xyz, device)
+    layer1, stats1 = _fps_prune_device(x, b[0], cfg, seeds)
+    layers, per_layer = [layer1], [stats1]
+    if cache_enabled:
+        stats1.cache_bytes = cache_footprint_bytes(b[0])
+        for m in b[1:]:
+            layers.append(BatchSample(layer1.indices[:, :m], layer1.selection_dist2[:, :m],
+                                      min(layer1.fill_boundary, m)))
+            per_layer.append(SamplerStats())
+    else:
+        for m in b[1:]:
+            s, st = run_restricted_batch(x, layers[-1].indices, m, 0)
+            layers.append(s)
+            per_layer.append(st)
+    total = SamplerStats(
+        distance_evals=sum(s.distance_evals for s in per_layer),
+        iterations=sum(s.iterations for s in per_layer),
+        candidates=sum(s.candidates for s in per_layer),
+        cache_bytes=sum(s.cache_bytes for s in per_layer))
+    return layers, total, per_layer
+
+
+def hierarchical_sample_host(points, budgets: Sequence[int], cfg: PruneConfig, seed_index=0,
+                             cache_enabled: bool = True, *, device=None, out=None):
+    """End-to-end call from HOST buffers: ``points`` (B, N, 3) float32/float64
+    numpy array or (preferably pinned) CPU tensor.  Copies the clouds to the
+    device, runs the pipeline, copies every layer's indices and selection
+    distances back and synchronises.  Returns (layers, total) with layers a
+    list of (indices int64 (B, M_l), selection_dist2 (B, M_l), fill_boundary)
+    host tensors; ``out`` may pass preallocated pinned (indices, sel) tensors
+    of shape (B, M1) for layer 1 (deeper cache-on layers are views of it)."""
+    dev = _device.require_cuda(device)
+    host = points if isinstance(points, torch.Tensor) else torch.from_numpy(
+        np.ascontiguousarray(points))
+    x = host.to(dev, non_blocking=host.is_pinned())
+    layers, total, _ = hierarchical_sample_batch(x, budgets, cfg, seed_index, cache_enabled)
+    res = []
+    if cache_enabled:
+        l1 = layers[0]
+        if out is not None:
+            hi, hs = out
+            hi.copy_(l1.indices, non_blocking=True)
+            hs.copy_(l1.selection_dist2, non_blocking=True)
+        else:
+            hi = l1.indices.to("cpu", non_blocking=False)
+            hs = l1.selection_dist2.to("cpu", non_blocking=False)
+        for s in layers:
+            m = len(s)
+            res.append((hi[:, :m], hs[:, :m], s.fill_boundary))
+    else:
+        for s in layers:
+            res.append((s.indices.to("cpu", non_blocking=True),
+                        s.selection_dist2.to("cpu", non_blocking=True), s.fill_boundary))
+    torch.cuda.current_stream(dev).synchronize()
+    return res, total

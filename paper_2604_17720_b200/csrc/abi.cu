@@ -1,0 +1,316 @@
+// C ABI (include/flashfps_b200.h): argument checks, kernel-configuration
+// planning and cluster launches.  No torch types cross this boundary.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <tuple>
+
+#include "../../include/flashfps_b200.h"
+#include "ffps_internal.h"
+
+namespace {
+
+thread_local std::string g_last_error;
+thread_local int64_t g_last_launches = 0;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+  return fail(FFPS_ECUDA, "%s: %s (%s)", what, cudaGetErrorName(e), cudaGetErrorString(e));
+}
+
+struct DeviceInfo {
+  int sms = 0;
+  size_t smem_optin = 0;
+};
+
+std::mutex g_mu;
+std::map<int, DeviceInfo> g_dev;
+std::map<std::tuple<int, const void*, int>, int> g_occ;  // (device, fn, C) -> max active clusters
+std::map<std::pair<int, const void*>, bool> g_attr_done;
+
+DeviceInfo device_info(int dev) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  auto it = g_dev.find(dev);
+  if (it != g_dev.end()) return it->second;
+  DeviceInfo d;
+  int v = 0;
+  cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+  d.sms = v;
+  cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  d.smem_optin = (size_t)v;
+  g_dev[dev] = d;
+  return d;
+}
+
+cudaError_t prepare_fn(int dev, const ffps::KernelInst& k) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  auto key = std::make_pair(dev, k.fn);
+  if (g_attr_done.count(key)) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(k.fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)k.smem_bytes);
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(k.fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  if (e != cudaSuccess) return e;
+  g_attr_done[key] = true;
+  return cudaSuccess;
+}
+
+int max_active_clusters(int dev, const ffps::KernelInst& k, int C) {
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    auto it = g_occ.find(std::make_tuple(dev, k.fn, C));
+    if (it != g_occ.end()) return it->second;
+  }
+  int result = 0;
+  if (prepare_fn(dev, k) == cudaSuccess) {
+    cudaLaunchConfig_t cfg;
+    memset(&cfg, 0, sizeof cfg);
+    cfg.gridDim = dim3(C * 64, 1, 1);
+    cfg.blockDim = dim3(k.nt, 1, 1);
+    cfg.dynamicSmemBytes = k.smem_bytes;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = C;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (cudaOccupancyMaxActiveClusters(&result, k.fn, &cfg) != cudaSuccess) {
+      cudaGetLastError();
+      result = 0;
+    }
+  } else {
+    cudaGetLastError();
+  }
+  std::lock_guard<std::mutex> lk(g_mu);
+  g_occ[std::make_tuple(dev, k.fn, C)] = result;
+  return result;
+}
+
+struct Plan {
+  const ffps::KernelInst* inst = nullptr;
+  int C = 0;
+  int G = 0;
+  int ctas_per_sm = 0;
+  int max_clusters = 0;
+};
+
+// Cost model (SM cycles per greedy iteration of the slowest wave):
+//   issue work of one CTA  W = NT * Q * c / 128   (c ~ 9.5 instr per register
+//                            slot, ~10.3 per smem slot, 4 warp-instr/clk/SM)
+//   exposed latency of the reduction + DSMEM push  L(C) = 450 + 25 C
+//   t_iter = max(W + L, r * W) with r resident CTAs per SM, times the waves.
+// FFPS_FORCE_PLAN="nt,p,s,C" overrides (benchmark sweeps).
+bool make_plan(int dev, int dtype, int64_t n, int64_t batch, Plan* out) {
+  const DeviceInfo di = device_info(dev);
+  int cnt = 0;
+  const ffps::KernelInst* insts = ffps::greedy_instances(&cnt);
+  const char* force = getenv("FFPS_FORCE_PLAN");
+  if (force && *force) {
+    int nt = 0, p = -1, s = -1, C = 0;
+    if (sscanf(force, "%d,%d,%d,%d", &nt, &p, &s, &C) == 4) {
+      for (int i = 0; i < cnt; ++i) {
+        const auto& k = insts[i];
+        if (k.dtype == dtype && k.nt == nt && k.p == p && k.s == s && C >= 1 && C <= 16) {
+          const int64_t cap = (int64_t)C * k.nt * (k.p + k.s);
+          const int64_t need = (n + (int64_t)C * k.nt - 1) / ((int64_t)C * k.nt);
+          out->inst = &k;
+          out->C = C;
+          out->G = cap >= n ? 0 : (int)(need - (k.p + k.s));
+          out->max_clusters = max_active_clusters(dev, k, C);
+          out->ctas_per_sm = k.minb;
+          return out->max_clusters > 0;
+        }
+      }
+    }
+  }
+  double best = 1e300;
+  for (int i = 0; i < cnt; ++i) {
+    const auto& k = insts[i];
+    if (k.dtype != dtype || k.smem_bytes > di.smem_optin) continue;
+    const int Q = k.p + k.s;
+    const int64_t per_cta = (int64_t)k.nt * Q;
+    const int64_t Cmin = (n + per_cta - 1) / per_cta;
+    if (Cmin > 16) continue;
+    const int C = (int)Cmin;
+    const int mc = max_active_clusters(dev, k, C);
+    if (mc <= 0) continue;
+    const double waves = std::ceil((double)batch / mc);
+    const int64_t resident = std::min<int64_t>(batch, mc) * C;
+    const int r = (int)std::min<int64_t>(k.minb, (resident + di.sms - 1) / di.sms);
+    const double c = (k.p * 9.5 + k.s * 10.3) / std::max(1, Q);
+    const double W = k.nt * Q * c / 128.0;
+    const double L = 450.0 + 25.0 * C;
+    const double t = std::max(W + L, r * W) * waves;
+    if (t < best * 0.999) {
+      best = t;
+      out->inst = &k;
+      out->C = C;
+      out->G = 0;
+      out->ctas_per_sm = r;
+      out->max_clusters = mc;
+    }
+  }
+  if (out->inst) return true;
+  // Spill: the largest on-chip configuration at 16 CTAs/cloud, the remainder
+  // of each thread's range streamed from global memory every iteration.
+  const ffps::KernelInst* big = nullptr;
+  for (int i = 0; i < cnt; ++i) {
+    const auto& k = insts[i];
+    if (k.dtype != dtype || k.smem_bytes > di.smem_optin) continue;
+    if (!big || (int64_t)k.nt * (k.p + k.s) * 4 / k.minb >
+                    (int64_t)big->nt * (big->p + big->s) * 4 / big->minb)
+      big = &k;
+  }
+  if (!big) return false;
+  const int C = 16;
+  const int64_t per_thread = (n + (int64_t)C * big->nt - 1) / ((int64_t)C * big->nt);
+  if (per_thread - (big->p + big->s) > (1 << 20)) return false;
+  out->inst = big;
+  out->C = C;
+  out->G = (int)(per_thread - (big->p + big->s));
+  out->max_clusters = max_active_clusters(dev, *big, C);
+  out->ctas_per_sm = big->minb;
+  return out->max_clusters > 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+int ffps_abi_version(void) { return FFPS_ABI_VERSION; }
+
+const char* ffps_last_error(void) { return g_last_error.c_str(); }
+
+int64_t ffps_last_launch_count(void) { return g_last_launches; }
+
+int ffps_plan(int dtype, int64_t n, int64_t batch, int64_t* out) {
+  if ((dtype != FFPS_F32 && dtype != FFPS_F64) || n < 1 || batch < 1 || !out)
+    return fail(FFPS_EINVAL, "ffps_plan: bad arguments");
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+  Plan p;
+  if (!make_plan(dev, dtype, n, batch, &p))
+    return fail(FFPS_EUNSUPPORTED, "no kernel configuration for n=%lld", (long long)n);
+  out[0] = p.inst->nt;
+  out[1] = p.inst->p;
+  out[2] = p.inst->s;
+  out[3] = p.G;
+  out[4] = p.C;
+  out[5] = p.ctas_per_sm;
+  out[6] = p.max_clusters;
+  return FFPS_OK;
+}
+
+int ffps_run_kernel(int dtype, const void* xyz, int64_t batch, int64_t cloud_stride, int64_t n,
+                    int64_t iters, const int64_t* seed_pos, const int64_t* index_map,
+                    int64_t map_stride, int64_t* order, void* sel_d2, int64_t out_stride,
+                    void* stream) {
+  g_last_launches = 0;
+  if (dtype != FFPS_F32 && dtype != FFPS_F64)
+    return fail(FFPS_EINVAL, "dtype must be FFPS_F32 or FFPS_F64");
+  if (batch < 0) return fail(FFPS_EINVAL, "batch=%lld < 0", (long long)batch);
+  if (batch == 0) return FFPS_OK;
+  if (!xyz || !seed_pos || !order || !sel_d2)
+    return fail(FFPS_EINVAL, "null device pointer");
+  if (n < 1 || n > 0x7fffffffLL) return fail(FFPS_EINVAL, "n=%lld out of range", (long long)n);
+  if (iters < 1 || iters > n)  // fps_core.py:178-180
+    return fail(FFPS_EINVAL, "m=%lld not in [1, %lld]", (long long)iters, (long long)n);
+  if (out_stride < iters) return fail(FFPS_EINVAL, "out_stride < iters");
+  if (index_map ? map_stride < n : cloud_stride < n)
+    return fail(FFPS_EINVAL, "cloud/map stride smaller than n");
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+  Plan plan;
+  if (!make_plan(dev, dtype, n, batch, &plan))
+    return fail(FFPS_EUNSUPPORTED, "no kernel configuration for n=%lld", (long long)n);
+  const ffps::KernelInst& k = *plan.inst;
+  e = prepare_fn(dev, k);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+
+  ffps::GreedyParams prm;
+  prm.xyz = xyz;
+  prm.cloud_stride = cloud_stride;
+  prm.index_map = index_map;
+  prm.map_stride = map_stride;
+  prm.n = n;
+  prm.iters = iters;
+  prm.seed_pos = seed_pos;
+  prm.order = order;
+  prm.sel_d2 = sel_d2;
+  prm.out_stride = out_stride;
+  prm.spill = nullptr;
+  prm.spill_slots = plan.G;
+  if (plan.G > 0) {
+    const size_t bytes =
+        ffps::spill_bytes_per_cta(dtype, k.nt, plan.G) * (size_t)plan.C * (size_t)batch;
+    e = cudaMallocAsync(&prm.spill, bytes, st);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync(spill)");
+  }
+
+  // Clusters of a batch beyond the device's resident capacity simply queue;
+  // each cluster is persistent for its own cloud.  Grid limit: 2^31-1 CTAs.
+  cudaLaunchConfig_t cfg;
+  memset(&cfg, 0, sizeof cfg);
+  cfg.gridDim = dim3((unsigned)(batch * plan.C), 1, 1);
+  cfg.blockDim = dim3(k.nt, 1, 1);
+  cfg.dynamicSmemBytes = k.smem_bytes;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = plan.C;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  void* args[] = {&prm};
+  e = cudaLaunchKernelExC(&cfg, k.fn, args);
+  if (e != cudaSuccess) {
+    if (prm.spill) cudaFreeAsync(prm.spill, st);
+    return cuda_fail(e, "fps_greedy_kernel launch");
+  }
+  g_last_launches = 1;
+  if (prm.spill) {
+    e = cudaFreeAsync(prm.spill, st);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaFreeAsync(spill)");
+  }
+  return FFPS_OK;
+}
+
+int ffps_fill_slice(int dtype, int64_t* order, void* sel_d2, int64_t batch, int64_t out_stride,
+                    int64_t k, int64_t m1, void* stream) {
+  g_last_launches = 0;
+  if (dtype != FFPS_F32 && dtype != FFPS_F64)
+    return fail(FFPS_EINVAL, "dtype must be FFPS_F32 or FFPS_F64");
+  if (batch < 0 || k < 1 || m1 < k || out_stride < m1)
+    return fail(FFPS_EINVAL, "fill: need 1 <= k <= m1 <= out_stride");
+  if (batch == 0 || m1 == k) return FFPS_OK;
+  if (!order || !sel_d2) return fail(FFPS_EINVAL, "null device pointer");
+  cudaError_t e = ffps::launch_fill_slice(dtype, order, sel_d2, batch, out_stride, k, m1,
+                                          static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "fill_slice_kernel launch");
+  g_last_launches = 1;
+  return FFPS_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,50 @@
+// Internal declarations shared by the kernel translation units and the C ABI.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <cstdint>
+
+namespace ffps {
+
+// Arguments of the persistent greedy kernel (one thread-block cluster per
+// cloud).  See include/flashfps_b200.h, ffps_run_kernel, for the meaning.
+struct GreedyParams {
+  const void* xyz;
+  int64_t cloud_stride;
+  const int64_t* index_map;
+  int64_t map_stride;
+  int64_t n;
+  int64_t iters;
+  const int64_t* seed_pos;
+  int64_t* order;
+  void* sel_d2;
+  int64_t out_stride;
+  void* spill;      // [batch][C][G][2?][NT] vectors, only when spill_slots > 0
+  int spill_slots;  // G: per-thread slots streamed from global memory
+};
+
+// One compiled configuration of the greedy kernel.
+struct KernelInst {
+  int dtype;  // 0 f32, 1 f64
+  int nt;     // threads per CTA
+  int p;      // register-resident slots per thread (xyz + dist in registers)
+  int s;      // smem-resident slots per thread (xyz in smem, dist in registers)
+  int minb;   // CTAs per SM the register budget is sized for (__launch_bounds__)
+  const void* fn;
+  size_t smem_bytes;  // dynamic shared memory per CTA
+};
+
+// All compiled configurations (fps_greedy.cu).
+const KernelInst* greedy_instances(int* count);
+
+// Spill-buffer bytes per (cloud, CTA) for G spill slots.
+inline size_t spill_bytes_per_cta(int dtype, int nt, int g) {
+  return static_cast<size_t>(g) * nt * (dtype == 0 ? 16 : 32);
+}
+
+// K2: slice fill (fill.cu).
+cudaError_t launch_fill_slice(int dtype, int64_t* order, void* sel_d2, int64_t batch,
+                              int64_t out_stride, int64_t k, int64_t m1, cudaStream_t st);
+
+}  // namespace ffps

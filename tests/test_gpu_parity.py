@@ -1,0 +1,248 @@
+"""Parity of the CUDA path (through the public API / C ABI) with the
+reference's golden vectors and with the CPU oracle.  Bar: bit-exact indices
+AND selection distances (integer/index work and exactly reproduced float
+arithmetic — no tolerance)."""
+
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2604_17720_b200 as ffps
+from paper_2604_17720_b200 import _native
+from oracle import oracle
+
+pytestmark = pytest.mark.gpu
+
+
+# ---------------------------------------------------------------- golden (fp64)
+def test_fps_matches_reference_goldens(golden, cuda):
+    for c in golden.cases("fps"):
+        cloud = ffps.PointCloud(golden.points(c))
+        s, st = ffps.fps(cloud, c["m"], c["seed"])
+        assert np.array_equal(s.indices, golden.out(c, "indices")), c["id"]
+        assert np.array_equal(s.selection_dist2, golden.out(c, "sel")), c["id"]
+        assert [st.distance_evals, st.iterations, st.candidates] == c["stats"]
+        assert s.fill_boundary == c["m"]
+
+
+def test_fps_prune_matches_reference_goldens(golden, cuda):
+    for c in golden.cases("prune"):
+        cfg = ffps.PruneConfig(p=c["p"], fill_mode=ffps.FillMode(c["fill"]),
+                               rng_seed=c.get("rng_seed", 0))
+        s, st = ffps.fps_prune(ffps.PointCloud(golden.points(c)), c["m1"], cfg, c["seed"])
+        assert np.array_equal(s.indices, golden.out(c, "indices")), c["id"]
+        assert np.array_equal(s.selection_dist2, golden.out(c, "sel")), c["id"]
+        assert s.fill_boundary == c["fill_boundary"]
+        assert [st.distance_evals, st.iterations, st.candidates] == c["stats"]
+
+
+def test_hierarchy_matches_reference_goldens(golden, cuda):
+    for c in golden.cases("hier"):
+        samples, st = ffps.hierarchical_sample(ffps.PointCloud(golden.points(c)), c["budgets"],
+                                               ffps.PruneConfig(p=c["p"]), c["seed"],
+                                               cache_enabled=c["cache"])
+        for li, s in enumerate(samples):
+            assert np.array_equal(s.indices, golden.out(c, f"L{li}_indices")), (c["id"], li)
+            assert np.array_equal(s.selection_dist2, golden.out(c, f"L{li}_sel")), (c["id"], li)
+        assert [s.fill_boundary for s in samples] == c["fill_boundaries"]
+        assert [st.distance_evals, st.iterations, st.candidates, st.cache_bytes] == c["stats"]
+
+
+def test_prefix_property_goldens(golden, cuda):
+    for c in golden.cases("prefix"):
+        res = ffps.verify_prefix_property(ffps.PointCloud(golden.points(c)), c["m1"], c["m2"],
+                                          c["seed"])
+        assert bool(res.ok) == c["ok"] and res.ok
+
+
+def test_fp32_goldens(golden, cuda):
+    for c in golden.cases("fps32"):
+        pts = torch.from_numpy(golden.points(c).astype(np.float32)).cuda()
+        s, _ = ffps.fps_batch(pts, c["m"], c["seed"])
+        assert s.selection_dist2.dtype == torch.float32
+        assert np.array_equal(s.indices[0].cpu().numpy(), golden.out(c, "indices")), c["id"]
+        assert np.array_equal(s.selection_dist2[0].cpu().numpy(), golden.out(c, "sel")), c["id"]
+
+
+# ------------------------------------------------------------ worked examples
+COLLINEAR = [(0, 0, 0), (1, 0, 0), (2, 0, 0), (3, 0, 0), (10, 0, 0)]
+
+
+def test_collinear_and_tiny_clouds(cuda):
+    s, st = ffps.fps(ffps.validate_cloud(COLLINEAR), 5, 0)
+    assert s.indices.tolist() == [0, 4, 3, 1, 2]
+    assert s.selection_dist2[1:].tolist() == [100.0, 9.0, 1.0, 1.0]
+    assert st.distance_evals == 20
+    s, st = ffps.fps(ffps.validate_cloud([(1, 2, 3)]), 1, 0)
+    assert s.indices.tolist() == [0] and np.isinf(s.selection_dist2[0])
+    assert st.distance_evals == 0
+    s, _ = ffps.fps(ffps.validate_cloud([(0, 0, 0), (5, 0, 0)]), 2, 0)
+    assert s.indices.tolist() == [0, 1] and s.selection_dist2[1] == 25.0
+    s, _ = ffps.fps_prune(ffps.validate_cloud(COLLINEAR), 5, ffps.PruneConfig(p=0.5), 0)
+    assert s.indices.tolist() == [0, 1, 2, 3, 4]
+
+
+# ------------------------------------------------- randomized vs the oracle
+def _check_batch(xyz, m, seeds, n=None, index_map=None):
+    xyz_d = torch.from_numpy(xyz).cuda()
+    B = xyz.shape[0]
+    if index_map is None:
+        nn = n or xyz.shape[1]
+        order = torch.empty((B, m), dtype=torch.int64, device="cuda")
+        sel = torch.empty((B, m), dtype=xyz_d.dtype, device="cuda")
+        from paper_2604_17720_b200 import _device
+        _device.greedy(xyz_d, nn, m, _device.seeds_tensor(seeds, B, "cuda"), order, sel)
+        go, gs = order.cpu().numpy(), sel.cpu().numpy()
+        wo, ws = oracle.run_kernel_batch(xyz, m, seeds, n=nn)
+    else:
+        s, _ = ffps.run_restricted_batch(xyz_d, torch.from_numpy(index_map).cuda(), m, seeds)
+        go, gs = s.indices.cpu().numpy(), s.selection_dist2.cpu().numpy()
+        wo, ws = oracle.run_kernel_batch(xyz, m, seeds, index_map=index_map)
+    for b in range(B):
+        bad = np.flatnonzero(go[b] != wo[b])
+        assert bad.size == 0, f"cloud {b}: first divergence at {bad[0]} of {m}"
+        assert np.array_equal(gs[b], ws[b]), f"cloud {b}: selection distances differ"
+
+
+def _cloud(rng, B, N, kind, dtype):
+    pts = rng.random((B, N, 3))
+    if kind == "ties":
+        for b in range(B):
+            dup = pts[b][rng.integers(0, N, size=N // 2)]
+            pts[b] = np.vstack([pts[b][: N - N // 2], dup])[rng.permutation(N)]
+    elif kind == "grid":  # massive exact ties of distances
+        g = np.stack(np.meshgrid(*(np.arange(12),) * 3, indexing="ij"), -1).reshape(-1, 3)
+        pts = np.broadcast_to(g[rng.permutation(len(g))[:N]] * 0.25, (B, N, 3)).copy()
+    elif kind == "collinear":
+        pts = np.zeros((B, N, 3))
+        pts[:, :, 0] = np.arange(N)
+    return np.ascontiguousarray(pts.astype(dtype))
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+@pytest.mark.parametrize("kind", ["uniform", "ties", "grid", "collinear"])
+def test_random_batches_vs_oracle(cuda, dtype, kind):
+    rng = np.random.default_rng(hash((kind, dtype().itemsize)) % 2**32)
+    for N, m, B in [(1, 1, 3), (2, 2, 2), (33, 33, 2), (257, 100, 3), (1000, 250, 4),
+                    (1728, 1728, 1), (5000, 1300, 3)]:
+        if kind == "grid" and N > 1728:
+            N = 1728
+        seeds = rng.integers(0, N, size=B)
+        _check_batch(_cloud(rng, B, N, kind, dtype), m, seeds)
+
+
+FORCED = {
+    np.float32: [("256,1,0,{C}", [1, 2, 3, 4, 7, 8, 16]), ("256,16,24,{C}", [1, 2, 5]),
+                 ("256,15,36,{C}", [1, 3, 4]), ("512,15,36,{C}", [1, 2]),
+                 ("256,8,0,{C}", [1, 16])],
+    np.float64: [("256,1,0,{C}", [1, 2, 5, 16]), ("256,8,8,{C}", [1, 3]),
+                 ("256,7,18,{C}", [1, 2, 4]), ("512,7,18,{C}", [1, 2])],
+}
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+def test_every_kernel_configuration(cuda, dtype, monkeypatch):
+    """Each compiled (threads, register slots, smem slots) configuration at
+    several cluster sizes, including forced spill (capacity < n)."""
+    rng = np.random.default_rng(7)
+    for fmt, clusters in FORCED[dtype]:
+        for C in clusters:
+            monkeypatch.setenv("FFPS_FORCE_PLAN", fmt.format(C=C))
+            nt, p, s, _ = (int(v) for v in fmt.format(C=C).split(","))
+            cap = nt * (p + s) * C
+            for N in sorted({max(2, cap // 3), cap, cap + 777}):   # last one spills
+                m = min(N, 97)
+                xyz = _cloud(rng, 2, N, "ties" if C % 2 else "uniform", dtype)
+                _check_batch(xyz, m, rng.integers(0, N, size=2))
+
+
+def test_restricted_runs_vs_oracle(cuda):
+    rng = np.random.default_rng(11)
+    for dtype in (np.float32, np.float64):
+        xyz = _cloud(rng, 3, 3000, "ties", dtype)
+        imap = np.stack([rng.permutation(3000)[:1200] for _ in range(3)])
+        _check_batch(xyz, 300, np.array([0, 5, 1199]), index_map=imap)
+
+
+def test_candidate_prefix_runs_vs_oracle(cuda):
+    rng = np.random.default_rng(12)
+    xyz = _cloud(rng, 4, 6000, "uniform", np.float32)
+    _check_batch(xyz, 375, np.zeros(4, np.int64), n=1500)
+
+
+@pytest.mark.parametrize("p", [0.0, 0.25, 0.5, 0.75, 0.9])
+@pytest.mark.parametrize("cache", [True, False])
+def test_hierarchy_batch_vs_oracle(cuda, p, cache):
+    rng = np.random.default_rng(int(p * 100) + cache)
+    budgets = (1500, 375, 93, 23)
+    xyz = _cloud(rng, 3, 6000, "uniform", np.float32)
+    layers, total, per = ffps.hierarchical_sample_batch(torch.from_numpy(xyz).cuda(), budgets,
+                                                        ffps.PruneConfig(p=p), 0,
+                                                        cache_enabled=cache)
+    for b in range(3):
+        want = oracle.hierarchical(xyz[b], budgets, p, 0, cache)
+        for li, (wi, ws) in enumerate(want):
+            assert np.array_equal(layers[li].indices[b].cpu().numpy(), wi), (b, li)
+            assert np.array_equal(layers[li].selection_dist2[b].cpu().numpy(), ws), (b, li)
+    k = oracle.kernel_budget(p, 1500)
+    c = oracle.candidate_count(p, 6000, 1500)
+    assert per[0].distance_evals == c * (k - 1) and layers[0].fill_boundary == k
+
+
+def test_random_fill_matches_reference_semantics(cuda):
+    rng = np.random.default_rng(5)
+    pts = rng.random((400, 3))
+    cfg = ffps.PruneConfig(p=0.5, fill_mode=ffps.FillMode.SEEDED_RANDOM, rng_seed=1)
+    a, _ = ffps.fps_prune(ffps.PointCloud(pts), 100, cfg, 0)
+    k = a.fill_boundary
+    order, _, _ = oracle.run_kernel(pts[:200], k, 0)
+    remaining = np.ones(400, bool)
+    remaining[order] = False
+    fill = np.random.default_rng(1).choice(np.flatnonzero(remaining), size=100 - k,
+                                           replace=False)
+    assert np.array_equal(a.indices, np.concatenate([order, fill]))
+    assert (a.selection_dist2[k:] == 0).all()
+
+
+def test_fill_slice_kernel_vs_oracle(cuda):
+    rng = np.random.default_rng(9)
+    for k, m1, n in [(1, 2, 10), (12, 50, 200), (1500, 6000, 24000), (70000, 300000, 300000)]:
+        B = 2
+        order = torch.full((B, m1), -1, dtype=torch.int64)
+        for b in range(B):
+            order[b, :k] = torch.from_numpy(rng.permutation(n)[:k])
+        od = order.cuda()
+        sd = torch.full((B, m1), 7.0, dtype=torch.float32, device="cuda")
+        from paper_2604_17720_b200 import _device
+        _device.fill_slice(od, sd, k, m1)
+        for b in range(B):
+            want = oracle.fill_slice(order[b, :k].numpy(), n, m1 - k)
+            assert np.array_equal(od[b, k:].cpu().numpy(), want), (k, m1, b)
+            assert (sd[b, k:] == 0).all() and (sd[b, :k] == 7.0).all()
+
+
+# ------------------------------------------------------------- error behaviour
+def test_errors_raised_before_device_work(cuda):
+    cloud = ffps.validate_cloud(COLLINEAR)
+    with pytest.raises(ffps.errors.BudgetOutOfRange):
+        ffps.fps(cloud, 0)
+    with pytest.raises(ffps.errors.BudgetOutOfRange):
+        ffps.fps(cloud, 6)
+    with pytest.raises(ffps.errors.SeedOutOfRange):
+        ffps.fps(cloud, 3, 5)
+    with pytest.raises(ffps.errors.SeedNotInCandidates):
+        ffps.fps_prune(ffps.PointCloud(np.random.default_rng(0).random((10, 3))), 4,
+                       ffps.PruneConfig(p=0.5), 7)
+    with pytest.raises(ffps.errors.BudgetExceedsCloud):
+        ffps.hierarchical_sample(cloud, (8, 2), ffps.PruneConfig())
+
+
+def test_abi_rejects_bad_arguments(cuda):
+    lib = _native.load()
+    rc = lib.ffps_run_kernel(0, 1, 1, 10, 10, 11, 1, None, 0, 1, 1, 11, None)
+    assert rc == -1 and b"not in" in lib.ffps_last_error()
+    rc = lib.ffps_run_kernel(7, 1, 1, 10, 10, 5, 1, None, 0, 1, 1, 5, None)
+    assert rc == -1
+    assert lib.ffps_fill_slice(0, 1, 1, 1, 10, 5, 4, None) == -1
