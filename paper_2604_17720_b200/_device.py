@@ -15,6 +15,28 @@ from .errors import KernelError
 
 _DTYPE_CODE = {torch.float32: _native.F32, torch.float64: _native.F64}
 _launches = 0
+_timers: list | None = None
+
+
+class kernel_timer:
+    """Context manager that brackets every K1 (greedy) launch issued inside it
+    with CUDA events on the launching stream; ``records`` holds
+    (batch, n, iters, start, end) tuples.  Used by bench.py to time the
+    dominant kernel live, inside the timed region."""
+
+    def __enter__(self):
+        global _timers
+        self.records = []
+        _timers = self.records
+        return self
+
+    def __exit__(self, *exc):
+        global _timers
+        _timers = None
+        return False
+
+    def kernel_ms(self):
+        return [(b, n, it, s.elapsed_time(e)) for b, n, it, s, e in self.records]
 
 
 def launches() -> int:
@@ -67,9 +89,17 @@ def greedy(xyz: torch.Tensor, n: int, iters: int, seeds: torch.Tensor,
         assert index_map.dtype == torch.int64 and index_map.stride(1) == 1
         map_ptr, map_stride = index_map.data_ptr(), index_map.stride(0)
     with torch.cuda.device(xyz.device):
+        if _timers is not None:
+            strm = torch.cuda.current_stream() if stream is None else stream
+            ev0 = torch.cuda.Event(enable_timing=True)
+            ev1 = torch.cuda.Event(enable_timing=True)
+            ev0.record(strm)
         _count(_native.run_kernel(dtype_code(xyz), xyz.data_ptr(), B, xyz.shape[1], n, iters,
                                   seeds.data_ptr(), map_ptr, map_stride, order.data_ptr(),
                                   sel.data_ptr(), order.stride(0), _stream_handle(stream)))
+        if _timers is not None:
+            ev1.record(strm)
+            _timers.append((B, n, iters, ev0, ev1))
 
 
 def fill_slice(order: torch.Tensor, sel: torch.Tensor, k: int, m1: int, stream=None) -> None:

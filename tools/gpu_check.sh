@@ -1,0 +1,10 @@
+mkdir -p gpurun_out
+set -x
+nvidia-smi -L; nproc; lscpu | grep "Model name"
+python -m pytest tests -m gpu -x -q > gpurun_out/pytest.log 2>&1; echo pytest=$?
+tail -3 gpurun_out/pytest.log
+timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo bench=$?
+cat gpurun_out/bench.json; tail -5 gpurun_out/bench.err
+B2="python bench.py --steps 2 --warmup 1 --no-cpu-baseline --exh-steps 1"
+timeout 600 $B2 > gpurun_out/b2.log 2>&1 && timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv $B2 > gpurun_out/ncu_launch.log 2>&1; echo ncu1=$?
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:fps_greedy -c 1 -o gpurun_out/prof_k1 $B2 > gpurun_out/ncu_full.log 2>&1; echo ncu2=$?
