@@ -45,8 +45,7 @@ std::map<int, DeviceInfo> g_dev;
 std::map<std::tuple<int, const void*, int>, int> g_occ;  // (device, fn, C) -> max active clusters
 std::map<std::pair<int, const void*>, bool> g_attr_done;
 
-DeviceInfo device_info(int dev) {
-  std::lock_guard<std::mutex> lk(g_mu);
+DeviceInfo device_info_nolock(int dev) {
   auto it = g_dev.find(dev);
   if (it != g_dev.end()) return it->second;
   DeviceInfo d;
@@ -59,12 +58,19 @@ DeviceInfo device_info(int dev) {
   return d;
 }
 
+DeviceInfo device_info(int dev) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  return device_info_nolock(dev);
+}
+
 cudaError_t prepare_fn(int dev, const ffps::KernelInst& k) {
   std::lock_guard<std::mutex> lk(g_mu);
   auto key = std::make_pair(dev, k.fn);
   if (g_attr_done.count(key)) return cudaSuccess;
-  cudaError_t e = cudaFuncSetAttribute(k.fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)k.smem_bytes);
+  const DeviceInfo di = device_info_nolock(dev);
+  cudaError_t e = cudaFuncSetAttribute(
+      k.fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      (int)std::min(k.smem_bytes(16), di.smem_optin));
   if (e != cudaSuccess) return e;
   e = cudaFuncSetAttribute(k.fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   if (e != cudaSuccess) return e;
@@ -84,7 +90,7 @@ int max_active_clusters(int dev, const ffps::KernelInst& k, int C) {
     memset(&cfg, 0, sizeof cfg);
     cfg.gridDim = dim3(C * 64, 1, 1);
     cfg.blockDim = dim3(k.nt, 1, 1);
-    cfg.dynamicSmemBytes = k.smem_bytes;
+    cfg.dynamicSmemBytes = k.smem_bytes(C);
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = C;
@@ -125,39 +131,46 @@ bool make_plan(int dev, int dtype, int64_t n, int64_t batch, Plan* out) {
   const char* force = getenv("FFPS_FORCE_PLAN");
   if (force && *force) {
     int nt = 0, p = -1, s = -1, C = 0;
-    if (sscanf(force, "%d,%d,%d,%d", &nt, &p, &s, &C) == 4) {
+    if (sscanf(force, "%d,%d,%d,%d", &nt, &p, &s, &C) == 4 && C >= 1 && C <= 16) {
+      const int64_t cap = (int64_t)C * nt * (p + s);
+      const bool spill = cap < n;
       for (int i = 0; i < cnt; ++i) {
         const auto& k = insts[i];
-        if (k.dtype == dtype && k.nt == nt && k.p == p && k.s == s && C >= 1 && C <= 16) {
-          const int64_t cap = (int64_t)C * k.nt * (k.p + k.s);
+        if (k.dtype == dtype && k.nt == nt && k.p == p && k.s == s && k.spill == spill) {
           const int64_t need = (n + (int64_t)C * k.nt - 1) / ((int64_t)C * k.nt);
           out->inst = &k;
           out->C = C;
-          out->G = cap >= n ? 0 : (int)(need - (k.p + k.s));
+          out->G = spill ? (int)(need - (k.p + k.s)) : 0;
           out->max_clusters = max_active_clusters(dev, k, C);
           out->ctas_per_sm = k.minb;
           return out->max_clusters > 0;
         }
       }
     }
+    return false;
   }
   double best = 1e300;
   for (int i = 0; i < cnt; ++i) {
     const auto& k = insts[i];
-    if (k.dtype != dtype || k.smem_bytes > di.smem_optin) continue;
+    if (k.dtype != dtype || k.spill) continue;
     const int Q = k.p + k.s;
     const int64_t per_cta = (int64_t)k.nt * Q;
     const int64_t Cmin = (n + per_cta - 1) / per_cta;
     if (Cmin > 16) continue;
     const int C = (int)Cmin;
+    if (k.smem_bytes(C) > di.smem_optin) continue;
     const int mc = max_active_clusters(dev, k, C);
     if (mc <= 0) continue;
     const double waves = std::ceil((double)batch / mc);
     const int64_t resident = std::min<int64_t>(batch, mc) * C;
     const int r = (int)std::min<int64_t>(k.minb, (resident + di.sms - 1) / di.sms);
-    const double c = (k.p * 9.5 + k.s * 10.3) / std::max(1, Q);
+    // issue cycles per point: ~5.5 (f32 packed) / ~10 (f64) plus an LDS per
+    // 4 (f32) / 2 (f64) smem points; 4 warp-instructions per clock per SM
+    const double cr = dtype == FFPS_F32 ? 5.5 : 10.0;
+    const double cs = cr + (dtype == FFPS_F32 ? 0.75 : 1.5);
+    const double c = (k.p * cr + k.s * cs) / std::max(1, Q);
     const double W = k.nt * Q * c / 128.0;
-    const double L = 450.0 + 25.0 * C;
+    const double L = 700.0 + 20.0 * C;
     const double t = std::max(W + L, r * W) * waves;
     if (t < best * 0.999) {
       best = t;
@@ -174,7 +187,7 @@ bool make_plan(int dev, int dtype, int64_t n, int64_t batch, Plan* out) {
   const ffps::KernelInst* big = nullptr;
   for (int i = 0; i < cnt; ++i) {
     const auto& k = insts[i];
-    if (k.dtype != dtype || k.smem_bytes > di.smem_optin) continue;
+    if (k.dtype != dtype || !k.spill || k.smem_bytes(16) > di.smem_optin) continue;
     if (!big || (int64_t)k.nt * (k.p + k.s) * 4 / k.minb >
                     (int64_t)big->nt * (big->p + big->s) * 4 / big->minb)
       big = &k;
@@ -261,6 +274,7 @@ int ffps_run_kernel(int dtype, const void* xyz, int64_t batch, int64_t cloud_str
   prm.out_stride = out_stride;
   prm.spill = nullptr;
   prm.spill_slots = plan.G;
+  prm.neg_zero = -0.0f;
   if (plan.G > 0) {
     const size_t bytes =
         ffps::spill_bytes_per_cta(dtype, k.nt, plan.G) * (size_t)plan.C * (size_t)batch;
@@ -274,7 +288,7 @@ int ffps_run_kernel(int dtype, const void* xyz, int64_t batch, int64_t cloud_str
   memset(&cfg, 0, sizeof cfg);
   cfg.gridDim = dim3((unsigned)(batch * plan.C), 1, 1);
   cfg.blockDim = dim3(k.nt, 1, 1);
-  cfg.dynamicSmemBytes = k.smem_bytes;
+  cfg.dynamicSmemBytes = k.smem_bytes(plan.C);
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;

@@ -22,6 +22,7 @@ struct GreedyParams {
   int64_t out_stride;
   void* spill;      // [batch][C][G][2?][NT] vectors, only when spill_slots > 0
   int spill_slots;  // G: per-thread slots streamed from global memory
+  float neg_zero;   // -0.0f, opaque to ptxas (see sq2 in fps_greedy.cu)
 };
 
 // One compiled configuration of the greedy kernel.
@@ -31,8 +32,11 @@ struct KernelInst {
   int p;      // register-resident slots per thread (xyz + dist in registers)
   int s;      // smem-resident slots per thread (xyz in smem, dist in registers)
   int minb;   // CTAs per SM the register budget is sized for (__launch_bounds__)
+  bool spill; // streams slots beyond P + S from a global spill buffer
   const void* fn;
-  size_t smem_bytes;  // dynamic shared memory per CTA
+  size_t smem_base;      // dynamic shared memory per CTA: points + mbarriers
+  size_t smem_per_rank;  // + exchange records per cluster rank
+  size_t smem_bytes(int C) const { return smem_base + (size_t)C * smem_per_rank; }
 };
 
 // All compiled configurations (fps_greedy.cu).

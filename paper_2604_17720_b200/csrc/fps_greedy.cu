@@ -10,32 +10,38 @@
 //     so "lowest thread, then lowest slot" == "lowest point index", which is
 //     the reference's tie rule (np.argmax first occurrence + chunk-order fold,
 //     fps_core.py:94, :98-107).
-//   * slots [0, P): x, y, z, dist in registers;
+//   * slots [0, P): x, y, z, dist in registers (pairs: float2 for FADD2/FMUL2);
 //     slots [P, P+S): x, y, z in shared memory (16-byte vectors, SoA by
 //     coordinate, conflict-free LDS.128), dist in registers;
 //     slots [P+S, Q): {x, y, z, dist} streamed from a global spill buffer
 //     (coalesced 16-byte loads) for clouds above on-chip capacity.
 //   * padding slots (index >= n) and the selected points hold dist = -inf,
 //     exactly like dist[best] = -inf in the reference (fps_core.py:169).
+//   * slots are grouped by 8; each group keeps its running max, so the
+//     winner search touches one group, not every slot.
 //
 // One iteration (everything below runs without host round trips):
 //   1. update   d = ((dx*dx + dy*dy) + dz*dz), every op separately rounded
-//               (RN, no FMA contraction — fps_core.py:74-83), dist = min(dist, d),
-//               thread max tm (3-input FMNMX) — the only per-point work.
-//   2. CTA max  REDUX.MAX over float bits (all live values are >= +0, so the
-//               signed-int order is the float order; -inf is negative) into a
-//               double-buffered smem slot, one __syncthreads.
-//   3. winner   the lowest warp / lane holding the CTA max scans its own slots
-//               for the lowest one equal to the max (lazy argmax: no per-point
-//               index bookkeeping) and pushes a record {max, index, x, y, z}
-//               into EVERY cluster peer's shared memory with st.async, which
-//               completes the peer's mbarrier transaction (DSMEM push; no
-//               cluster-wide barrier per iteration).
-//   4. combine  every thread waits on its CTA's mbarrier for C records, takes
-//               max value / lowest index, and gets the next point's xyz from
-//               the record; the owning thread marks dist = -inf.
-// Records and maxima are double-buffered by iteration parity, so a single
-// __syncthreads + one mbarrier wait per iteration is all the synchronisation.
+//               (RN, no FMA contraction — fps_core.py:74-83).  For fp32 two
+//               points go through one packed f32x2 sub/mul/add (FADD2/FMUL2,
+//               per-lane IEEE RN, bit-identical to the scalar ops);
+//               dist = min(dist, d); group max via 3-input FMNMX.
+//   2. warp     REDUX.MAX over the float bits (every live value is >= +0, so
+//               the signed-int order is the float order; -inf is negative),
+//               ballot for the lowest lane holding it, that lane finds its
+//               lowest group/slot with the max (lazy argmax: no per-point
+//               index bookkeeping) and the record {max, index, x, y, z} is
+//               pushed by lanes 0..C-1 into EVERY cluster peer's shared
+//               memory with st.async, completing the peer's mbarrier
+//               transaction (DSMEM push; no __syncthreads, no cluster barrier).
+//   3. combine  each warp waits on its CTA's mbarrier for the C*NW records,
+//               reduces them (max value, then lowest index) with two warp
+//               reductions and reads the winner's xyz; the owning thread marks
+//               its slot dist = -inf.
+// Records are double-buffered by iteration parity: a peer can only push
+// iteration k+2 after every warp of this CTA pushed k+1, i.e. after they all
+// consumed iteration k's records — one mbarrier wait per warp per iteration
+// is the only synchronisation.
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -45,23 +51,77 @@
 
 namespace ffps {
 
+constexpr int kGroup = 8;  // slots per running-max group
+
+// ---- packed f32x2 arithmetic (sm_100: FADD2 / FMUL2, IEEE RN per lane) ----
+__device__ __forceinline__ float2 sub2(float2 a, float2 b) {
+  float2 r;
+  asm("{.reg .b64 a, b, d;\n\t"
+      "mov.b64 a, {%2, %3};\n\tmov.b64 b, {%4, %5};\n\t"
+      "sub.rn.f32x2 d, a, b;\n\tmov.b64 {%0, %1}, d;}"
+      : "=f"(r.x), "=f"(r.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return r;
+}
+// a*a + z with z = -0.0 supplied at RUN time (GreedyParams::neg_zero): equal to
+// the separately rounded square RN(a*a) for every a (adding -0 to the exact
+// product changes nothing, and +0 + -0 = +0).  A plain mul.rn.f32x2 followed
+// by add.rn.f32x2 is contracted into FFMA2 by ptxas 12.9 even with
+// --fmad=false, which would round (a*a + b) once and break bit-exactness; an
+// addend ptxas cannot prove to be -0 keeps the square a separate FFMA2.
+__device__ __forceinline__ float2 sq2(float2 a, float2 z) {
+  float2 r;
+  asm("{.reg .b64 a, z, d;\n\t"
+      "mov.b64 a, {%2, %3};\n\tmov.b64 z, {%4, %5};\n\t"
+      "fma.rn.f32x2 d, a, a, z;\n\tmov.b64 {%0, %1}, d;}"
+      : "=f"(r.x), "=f"(r.y)
+      : "f"(a.x), "f"(a.y), "f"(z.x), "f"(z.y));
+  return r;
+}
+__device__ __forceinline__ float2 add2(float2 a, float2 b) {
+  float2 r;
+  asm("{.reg .b64 a, b, d;\n\t"
+      "mov.b64 a, {%2, %3};\n\tmov.b64 b, {%4, %5};\n\t"
+      "add.rn.f32x2 d, a, b;\n\tmov.b64 {%0, %1}, d;}"
+      : "=f"(r.x), "=f"(r.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return r;
+}
+__device__ __forceinline__ float max3f(float a, float b, float c) {
+  float r;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
+
 template <typename T>
 struct Arith;
 
 template <>
 struct Arith<float> {
   using bits_t = int32_t;
+  using pair_t = float2;
   using vec_t = float4;
-  static constexpr int VW = 4;             // slots per 16-byte vector
+  static constexpr int VW = 4;             // slots per 16-byte smem vector
   static constexpr int REC_STRIDE = 32;    // bytes per exchange record in smem
   static constexpr uint32_t REC_TX = 20;   // bytes pushed per record
   __device__ static __forceinline__ float pinf() { return __int_as_float(0x7f800000); }
   __device__ static __forceinline__ float ninf() { return __int_as_float(0xff800000); }
+  __device__ static __forceinline__ pair_t mk(float a, float b) { return make_float2(a, b); }
   // fps_core.py:74-83: ((xs-px)^2 + (ys-py)^2) + (zs-pz)^2, separately rounded
   __device__ static __forceinline__ float d2(float x, float y, float z, float px, float py,
                                              float pz) {
     const float dx = __fsub_rn(x, px), dy = __fsub_rn(y, py), dz = __fsub_rn(z, pz);
     return __fadd_rn(__fadd_rn(__fmul_rn(dx, dx), __fmul_rn(dy, dy)), __fmul_rn(dz, dz));
+  }
+  // two points at once: d = min(d, d2(p)), gm = max(gm, d.x, d.y); nz = (-0, -0)
+  __device__ static __forceinline__ void upd2(pair_t& d, pair_t x, pair_t y, pair_t z,
+                                              pair_t px, pair_t py, pair_t pz, pair_t nz,
+                                              float& gm) {
+    const float2 dx = sub2(x, px), dy = sub2(y, py), dz = sub2(z, pz);
+    const float2 s = add2(add2(sq2(dx, nz), sq2(dy, nz)), sq2(dz, nz));
+    d.x = fminf(d.x, s.x);
+    d.y = fminf(d.y, s.y);
+    gm = max3f(gm, d.x, d.y);
   }
   __device__ static __forceinline__ float vmin(float a, float b) { return fminf(a, b); }
   __device__ static __forceinline__ float vmax(float a, float b) { return fmaxf(a, b); }
@@ -70,11 +130,8 @@ struct Arith<float> {
   __device__ static __forceinline__ bits_t warp_max(bits_t v) {
     return __reduce_max_sync(0xffffffffu, v);
   }
-  __device__ static __forceinline__ vec_t pack(const float* a) {
-    return make_float4(a[0], a[1], a[2], a[3]);
-  }
-  __device__ static __forceinline__ void unpack(const vec_t& v, float* a) {
-    a[0] = v.x; a[1] = v.y; a[2] = v.z; a[3] = v.w;
+  __device__ static __forceinline__ bits_t shfl(bits_t v, int l) {
+    return __shfl_sync(0xffffffffu, v, l);
   }
   // spill slot s: one float4 {x, y, z, dist}
   __device__ static __forceinline__ void spill_load(const vec_t* sp, int s, int nt, int tid,
@@ -90,15 +147,16 @@ struct Arith<float> {
                                                        float d) {
     reinterpret_cast<float*>(sp + (size_t)s * nt + tid)[3] = d;
   }
-  __device__ static __forceinline__ void send(uint32_t raddr, uint32_t rbar, bits_t v, int64_t g,
-                                              float x, float y, float z) {
-    st_async_v4(raddr, rbar, (uint32_t)v, (uint32_t)g, __float_as_uint(x), __float_as_uint(y));
+  // record: {value bits, index, x, y} + {z}
+  __device__ static __forceinline__ void send(uint32_t raddr, uint32_t rbar, bits_t v,
+                                              uint32_t g, float x, float y, float z) {
+    st_async_v4(raddr, rbar, (uint32_t)v, g, __float_as_uint(x), __float_as_uint(y));
     st_async_b32(raddr + 16, rbar, __float_as_uint(z));
   }
-  __device__ static __forceinline__ void recv(const unsigned char* rec, bits_t& v, int64_t& g) {
+  __device__ static __forceinline__ void recv(const unsigned char* rec, bits_t& v, uint32_t& g) {
     const int2 a = *reinterpret_cast<const int2*>(rec);
     v = a.x;
-    g = (int64_t)(uint32_t)a.y;
+    g = (uint32_t)a.y;
   }
   __device__ static __forceinline__ void recv_xyz(const unsigned char* rec, float& x, float& y,
                                                   float& z) {
@@ -111,32 +169,39 @@ struct Arith<float> {
 template <>
 struct Arith<double> {
   using bits_t = long long;
+  using pair_t = double2;
   using vec_t = double2;
   static constexpr int VW = 2;
   static constexpr int REC_STRIDE = 48;
   static constexpr uint32_t REC_TX = 40;
   __device__ static __forceinline__ double pinf() { return __longlong_as_double(0x7ff0000000000000ll); }
   __device__ static __forceinline__ double ninf() { return __longlong_as_double((long long)0xfff0000000000000ull); }
+  __device__ static __forceinline__ pair_t mk(double a, double b) { return make_double2(a, b); }
   __device__ static __forceinline__ double d2(double x, double y, double z, double px,
                                               double py, double pz) {
     const double dx = __dsub_rn(x, px), dy = __dsub_rn(y, py), dz = __dsub_rn(z, pz);
     return __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
+  }
+  __device__ static __forceinline__ void upd2(pair_t& d, pair_t x, pair_t y, pair_t z,
+                                              pair_t px, pair_t py, pair_t pz, pair_t,
+                                              double& gm) {
+    d.x = fmin(d.x, d2(x.x, y.x, z.x, px.x, py.x, pz.x));
+    d.y = fmin(d.y, d2(x.y, y.y, z.y, px.y, py.y, pz.y));
+    gm = fmax(gm, fmax(d.x, d.y));
   }
   __device__ static __forceinline__ double vmin(double a, double b) { return fmin(a, b); }
   __device__ static __forceinline__ double vmax(double a, double b) { return fmax(a, b); }
   __device__ static __forceinline__ bits_t bits(double v) { return __double_as_longlong(v); }
   __device__ static __forceinline__ double from_bits(bits_t b) { return __longlong_as_double(b); }
   __device__ static __forceinline__ bits_t warp_max(bits_t v) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const bits_t u = __shfl_xor_sync(0xffffffffu, v, o);
-      v = u > v ? u : v;
-    }
-    return v;
+    // max of signed 64-bit keys: high word first (signed), then low word
+    const int hi = __reduce_max_sync(0xffffffffu, (int)(v >> 32));
+    const unsigned lo_c = ((int)(v >> 32) == hi) ? (unsigned)(v & 0xffffffffu) : 0u;
+    const unsigned lo = __reduce_max_sync(0xffffffffu, lo_c);
+    return (long long)(((unsigned long long)(unsigned)hi << 32) | lo);
   }
-  __device__ static __forceinline__ vec_t pack(const double* a) { return make_double2(a[0], a[1]); }
-  __device__ static __forceinline__ void unpack(const vec_t& v, double* a) {
-    a[0] = v.x; a[1] = v.y;
+  __device__ static __forceinline__ bits_t shfl(bits_t v, int l) {
+    return __shfl_sync(0xffffffffu, v, l);
   }
   // spill slot s: two double2 {x, y}, {z, dist}
   __device__ static __forceinline__ void spill_load(const vec_t* sp, int s, int nt, int tid,
@@ -154,17 +219,18 @@ struct Arith<double> {
                                                        double d) {
     reinterpret_cast<double*>(sp + (size_t)(2 * s + 1) * nt + tid)[1] = d;
   }
-  __device__ static __forceinline__ void send(uint32_t raddr, uint32_t rbar, bits_t v, int64_t g,
-                                              double x, double y, double z) {
+  // record: {value bits, index} + {x, y} + {z}
+  __device__ static __forceinline__ void send(uint32_t raddr, uint32_t rbar, bits_t v,
+                                              uint32_t g, double x, double y, double z) {
     st_async_v2_b64(raddr, rbar, (uint64_t)v, (uint64_t)g);
     st_async_v2_b64(raddr + 16, rbar, (uint64_t)__double_as_longlong(x),
                     (uint64_t)__double_as_longlong(y));
     st_async_b64(raddr + 32, rbar, (uint64_t)__double_as_longlong(z));
   }
-  __device__ static __forceinline__ void recv(const unsigned char* rec, bits_t& v, int64_t& g) {
+  __device__ static __forceinline__ void recv(const unsigned char* rec, bits_t& v, uint32_t& g) {
     const longlong2 a = *reinterpret_cast<const longlong2*>(rec);
     v = a.x;
-    g = a.y;
+    g = (uint32_t)a.y;
   }
   __device__ static __forceinline__ void recv_xyz(const unsigned char* rec, double& x, double& y,
                                                   double& z) {
@@ -174,57 +240,55 @@ struct Arith<double> {
   }
 };
 
-constexpr int kMaxCluster = 16;
-
+// shared memory: [SG][3][NT] coordinate vectors, then 2 mbarriers (16 B),
+// then the exchange records [2 parities][C ranks][NW warps] (sized per launch)
 template <typename T, int NT>
-__host__ __device__ constexpr size_t tail_offset_red() { return 16; }
-template <typename T, int NT>
-__host__ __device__ constexpr size_t tail_offset_xch() {
-  return (16 + 2 * (NT / 32) * sizeof(typename Arith<T>::bits_t) + 15) / 16 * 16;
-}
-template <typename T, int NT>
-__host__ __device__ constexpr size_t tail_bytes() {
-  return tail_offset_xch<T, NT>() + 2 * kMaxCluster * Arith<T>::REC_STRIDE;
+__host__ __device__ constexpr size_t rec_bytes_per_rank() {
+  return 2 * (size_t)(NT / 32) * Arith<T>::REC_STRIDE;
 }
 
-template <typename T, int NT, int P, int S, int MINB>
+template <typename T, int NT, int P, int S, int MINB, bool SPILL>
 __global__ void __launch_bounds__(NT, MINB) fps_greedy_kernel(const GreedyParams prm) {
   using A = Arith<T>;
   using bits_t = typename A::bits_t;
+  using pair_t = typename A::pair_t;
   using vec_t = typename A::vec_t;
   constexpr int VW = A::VW;
-  static_assert(S % VW == 0, "smem slots must fill whole 16-byte vectors");
-  constexpr int SG = S / VW;
+  static_assert(P % 2 == 0, "register slots come in pairs");
+  static_assert(S % VW == 0 && S % 2 == 0, "smem slots must fill whole 16-byte vectors");
+  constexpr int SG = S / VW;      // smem vectors per coordinate
   constexpr int NW = NT / 32;
   constexpr int RS = A::REC_STRIDE;
+  constexpr int GR = (P + kGroup - 1) / kGroup;  // register-slot groups
+  constexpr int GM = (S + kGroup - 1) / kGroup;  // smem-slot groups
+  constexpr int NG = (GR + GM) > 0 ? (GR + GM) : 1;
 
   extern __shared__ __align__(16) unsigned char smem[];
   vec_t* sv = reinterpret_cast<vec_t*>(smem);  // [SG][3][NT]
   unsigned char* tail = smem + (size_t)SG * 3 * NT * sizeof(vec_t);
-  bits_t* red = reinterpret_cast<bits_t*>(tail + tail_offset_red<T, NT>());  // [2][NW]
-  unsigned char* xch = tail + tail_offset_xch<T, NT>();                      // [2][16][RS]
-  const uint32_t mbar0 = smem_u32(tail);                                     // 2 x u64
+  unsigned char* xch = tail + 16;               // [2][C][NW][RS]
+  const uint32_t mbar0 = smem_u32(tail);        // 2 x u64
 
   const uint32_t C = cluster_nctarank();
   const uint32_t rank = cluster_ctarank();
   const int64_t b = cluster_id_x();
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int G = prm.spill_slots;
-  const int64_t Q = P + S + G;
-  const int64_t base = ((int64_t)rank * NT + tid) * Q;
-  const int64_t n = prm.n;
+  // all point positions are < 2^31 (checked by the C ABI): 32-bit loop state
+  const int G = SPILL ? prm.spill_slots : 0;
+  const int Q = P + S + G;
+  const int base = ((int)rank * NT + tid) * Q;
+  const int n = (int)prm.n;
+  const int iters = (int)prm.iters;
   const T* X = static_cast<const T*>(prm.xyz) + b * prm.cloud_stride * 3;
   const int64_t* map = prm.index_map ? prm.index_map + b * prm.map_stride : nullptr;
-  const int64_t seed = prm.seed_pos[b];
-  int64_t* order = prm.order + b * prm.out_stride;
-  T* sel = static_cast<T*>(prm.sel_d2) + b * prm.out_stride;
+  const int seed = (int)prm.seed_pos[b];
   vec_t* spill = nullptr;
-  if (G > 0)
+  if (SPILL)
     spill = static_cast<vec_t*>(prm.spill) +
             (size_t)(b * C + rank) * (size_t)G * (sizeof(T) == 4 ? 1 : 2) * NT;
 
   // ---- load the owned range (fps_core.py:119-130: dist=+inf, dist[seed]=-inf)
-  auto fetch = [&](int64_t i, T& x, T& y, T& z, T& d) {
+  auto fetch = [&](int i, T& x, T& y, T& z, T& d) {
     if (i < n) {
       const int64_t src = map ? __ldg(map + i) : i;
       x = X[3 * src + 0];
@@ -237,18 +301,36 @@ __global__ void __launch_bounds__(NT, MINB) fps_greedy_kernel(const GreedyParams
     }
   };
 
-  T rx[P > 0 ? P : 1], ry[P > 0 ? P : 1], rz[P > 0 ? P : 1], rd[P > 0 ? P : 1];
-  T sd[S > 0 ? S : 1];
+  constexpr int P2 = P > 0 ? P / 2 : 1;
+  constexpr int S2 = S > 0 ? S / 2 : 1;
+  pair_t rx[P2], ry[P2], rz[P2], rd[P2];
+  pair_t sd[S2];
 #pragma unroll
-  for (int j = 0; j < P; ++j) fetch(base + j, rx[j], ry[j], rz[j], rd[j]);
+  for (int j = 0; j < P / 2; ++j) {
+    T x0, y0, z0, d0, x1, y1, z1, d1;
+    fetch(base + 2 * j, x0, y0, z0, d0);
+    fetch(base + 2 * j + 1, x1, y1, z1, d1);
+    rx[j] = A::mk(x0, x1);
+    ry[j] = A::mk(y0, y1);
+    rz[j] = A::mk(z0, z1);
+    rd[j] = A::mk(d0, d1);
+  }
 #pragma unroll
   for (int q = 0; q < SG; ++q) {
-    T xs[VW], ys[VW], zs[VW];
+    T xs[VW], ys[VW], zs[VW], ds[VW];
 #pragma unroll
-    for (int v = 0; v < VW; ++v) fetch(base + P + q * VW + v, xs[v], ys[v], zs[v], sd[q * VW + v]);
-    sv[(q * 3 + 0) * NT + tid] = A::pack(xs);
-    sv[(q * 3 + 1) * NT + tid] = A::pack(ys);
-    sv[(q * 3 + 2) * NT + tid] = A::pack(zs);
+    for (int v = 0; v < VW; ++v) fetch(base + P + q * VW + v, xs[v], ys[v], zs[v], ds[v]);
+#pragma unroll
+    for (int v = 0; v < VW; v += 2) sd[(q * VW + v) / 2] = A::mk(ds[v], ds[v + 1]);
+    T* sx = reinterpret_cast<T*>(&sv[(q * 3 + 0) * NT + tid]);
+    T* sy = reinterpret_cast<T*>(&sv[(q * 3 + 1) * NT + tid]);
+    T* sz = reinterpret_cast<T*>(&sv[(q * 3 + 2) * NT + tid]);
+#pragma unroll
+    for (int v = 0; v < VW; ++v) {
+      sx[v] = xs[v];
+      sy[v] = ys[v];
+      sz[v] = zs[v];
+    }
   }
   for (int s = 0; s < G; ++s) {
     T x, y, z, d;
@@ -264,8 +346,8 @@ __global__ void __launch_bounds__(NT, MINB) fps_greedy_kernel(const GreedyParams
     pz = X[3 * src + 2];
   }
   if (rank == 0 && tid == 0) {
-    order[0] = seed;
-    sel[0] = A::pinf();
+    prm.order[b * prm.out_stride] = seed;
+    static_cast<T*>(prm.sel_d2)[b * prm.out_stride] = A::pinf();
   }
   if (tid == 0) {
     mbar_init(mbar0, 1);
@@ -275,77 +357,90 @@ __global__ void __launch_bounds__(NT, MINB) fps_greedy_kernel(const GreedyParams
   cluster_sync_all();  // mbarriers initialised cluster-wide; smem points visible
 
   const uint32_t xch0 = smem_u32(xch);
-  for (int64_t k = 1; k < prm.iters; ++k) {
+  const uint32_t nrec = C * NW;
+  for (int k = 1; k < iters; ++k) {
     const uint32_t par = (uint32_t)((k - 1) & 1);
     const uint32_t phase = (uint32_t)(((k - 1) >> 1) & 1);
     const uint32_t bar = mbar0 + 8 * par;
+    if (tid == 0) mbar_arrive_expect_tx(bar, nrec * A::REC_TX);
 
-    // 1. fused distance update + thread max -----------------------------------
-    T tm0 = A::ninf(), tm1 = A::ninf();
+    // 1. fused distance update + per-group running max --------------------------
+    const pair_t ppx = A::mk(px, px), ppy = A::mk(py, py), ppz = A::mk(pz, pz);
+    const pair_t nz = A::mk((T)prm.neg_zero, (T)prm.neg_zero);
+    T gm[NG];
 #pragma unroll
-    for (int j = 0; j < P; ++j) {
-      rd[j] = A::vmin(rd[j], A::d2(rx[j], ry[j], rz[j], px, py, pz));
-      if (j & 1) tm1 = A::vmax(tm1, rd[j]);
-      else tm0 = A::vmax(tm0, rd[j]);
-    }
+    for (int g = 0; g < NG; ++g) gm[g] = A::ninf();
+#pragma unroll
+    for (int j = 0; j < P / 2; ++j)
+      A::upd2(rd[j], rx[j], ry[j], rz[j], ppx, ppy, ppz, nz, gm[(2 * j) / kGroup]);
 #pragma unroll
     for (int q = 0; q < SG; ++q) {
-      T xs[VW], ys[VW], zs[VW];
-      A::unpack(sv[(q * 3 + 0) * NT + tid], xs);
-      A::unpack(sv[(q * 3 + 1) * NT + tid], ys);
-      A::unpack(sv[(q * 3 + 2) * NT + tid], zs);
+      const vec_t vx = sv[(q * 3 + 0) * NT + tid];
+      const vec_t vy = sv[(q * 3 + 1) * NT + tid];
+      const vec_t vz = sv[(q * 3 + 2) * NT + tid];
+      const T* ax = reinterpret_cast<const T*>(&vx);
+      const T* ay = reinterpret_cast<const T*>(&vy);
+      const T* az = reinterpret_cast<const T*>(&vz);
 #pragma unroll
-      for (int v = 0; v < VW; ++v) {
-        T& d = sd[q * VW + v];
-        d = A::vmin(d, A::d2(xs[v], ys[v], zs[v], px, py, pz));
-        if (v & 1) tm1 = A::vmax(tm1, d);
-        else tm0 = A::vmax(tm0, d);
+      for (int v = 0; v < VW; v += 2) {
+        const int j = q * VW + v;  // smem slot
+        A::upd2(sd[j / 2], A::mk(ax[v], ax[v + 1]), A::mk(ay[v], ay[v + 1]),
+                A::mk(az[v], az[v + 1]), ppx, ppy, ppz, nz, gm[GR + j / kGroup]);
       }
     }
-    for (int s = 0; s < G; ++s) {
+    T gsp = A::ninf();
+    for (int s = 0; SPILL && s < G; ++s) {
       T x, y, z, d;
       A::spill_load(spill, s, NT, tid, x, y, z, d);
       const T nd = A::vmin(d, A::d2(x, y, z, px, py, pz));
       A::spill_store_d(spill, s, NT, tid, nd);
-      tm0 = A::vmax(tm0, nd);
+      gsp = A::vmax(gsp, nd);
     }
-    const bits_t tb = A::bits(A::vmax(tm0, tm1));
+    T tm = gsp;
+#pragma unroll
+    for (int g = 0; g < NG; ++g) tm = A::vmax(tm, gm[g]);
+    const bits_t tb = A::bits(tm);
 
-    // 2. CTA max ----------------------------------------------------------------
+    // 2. warp max, lowest lane holding it finds its lowest slot ---------------
     const bits_t wb = A::warp_max(tb);
-    if (lane == 0) red[par * NW + warp] = wb;
-    __syncthreads();
-    bits_t cb = red[par * NW];
-    int ws = 0;
+    const unsigned bal = __ballot_sync(0xffffffffu, tb == wb);
+    const int wl = __ffs(bal) - 1;
+    uint32_t widx = 0;
+    T cx = T(0), cy = T(0), cz = T(0);
+    if (lane == wl) {
+      int gsel = NG;  // NG = spill group
 #pragma unroll
-    for (int w = 1; w < NW; ++w) {
-      const bits_t v = red[par * NW + w];
-      if (v > cb) {
-        cb = v;
-        ws = w;
-      }
-    }
-    if (tid == 0) mbar_arrive_expect_tx(bar, C * A::REC_TX);
-
-    // 3. lowest holder of the CTA max finds its lowest slot and pushes the record
-    if (warp == ws) {
-      const unsigned bal = __ballot_sync(0xffffffffu, tb == cb);
-      if (lane == __ffs(bal) - 1) {
-        int jj = -1;
-        T cx = T(0), cy = T(0), cz = T(0);
+      for (int g = NG - 1; g >= 0; --g)
+        if (A::bits(gm[g]) == wb) gsel = g;
+      int jj = -1;
 #pragma unroll
-        for (int j = P - 1; j >= 0; --j)
-          if (A::bits(rd[j]) == cb) {
-            jj = j;
-            cx = rx[j];
-            cy = ry[j];
-            cz = rz[j];
+      for (int g = 0; g < GR; ++g) {
+        if (g == gsel) {
+#pragma unroll
+          for (int j = (g * kGroup + kGroup < P ? g * kGroup + kGroup : P) - 1; j >= g * kGroup;
+               --j) {
+            const pair_t dd = rd[j / 2];
+            const T dv = (j & 1) ? dd.y : dd.x;
+            if (A::bits(dv) == wb) {
+              jj = j;
+              cx = (j & 1) ? rx[j / 2].y : rx[j / 2].x;
+              cy = (j & 1) ? ry[j / 2].y : ry[j / 2].x;
+              cz = (j & 1) ? rz[j / 2].y : rz[j / 2].x;
+            }
           }
-        if (jj < 0) {
+        }
+      }
+#pragma unroll
+      for (int g = 0; g < GM; ++g) {
+        if (GR + g == gsel) {
           int js = -1;
 #pragma unroll
-          for (int j = S - 1; j >= 0; --j)
-            if (A::bits(sd[j]) == cb) js = j;
+          for (int j = (g * kGroup + kGroup < S ? g * kGroup + kGroup : S) - 1; j >= g * kGroup;
+               --j) {
+            const pair_t dd = sd[j / 2];
+            const T dv = (j & 1) ? dd.y : dd.x;
+            if (A::bits(dv) == wb) js = j;
+          }
           if (js >= 0) {
             jj = P + js;
             const int q = js / VW, v = js % VW;
@@ -353,69 +448,91 @@ __global__ void __launch_bounds__(NT, MINB) fps_greedy_kernel(const GreedyParams
             cx = sc[((size_t)(q * 3 + 0) * NT + tid) * VW + v];
             cy = sc[((size_t)(q * 3 + 1) * NT + tid) * VW + v];
             cz = sc[((size_t)(q * 3 + 2) * NT + tid) * VW + v];
-          } else {
-            for (int s = 0; s < G; ++s) {
-              T x, y, z, d;
-              A::spill_load(spill, s, NT, tid, x, y, z, d);
-              if (A::bits(d) == cb) {
-                jj = P + S + s;
-                cx = x;
-                cy = y;
-                cz = z;
-                break;
-              }
-            }
           }
         }
-        const int64_t g = base + jj;
-        const uint32_t slot = xch0 + (par * kMaxCluster + rank) * RS;
-        for (uint32_t r = 0; r < C; ++r) A::send(mapa(slot, r), mapa(bar, r), cb, g, cx, cy, cz);
       }
+      if (SPILL && gsel == NG) {
+        for (int s = 0; s < G; ++s) {
+          T x, y, z, d;
+          A::spill_load(spill, s, NT, tid, x, y, z, d);
+          if (A::bits(d) == wb) {
+            jj = P + S + s;
+            cx = x;
+            cy = y;
+            cz = z;
+            break;
+          }
+        }
+      }
+      widx = (uint32_t)(base + (jj < 0 ? 0 : jj));
+    }
+    // hand the record to lanes 0..C-1, which push it to the C peers in parallel
+    widx = __shfl_sync(0xffffffffu, widx, wl);
+    cx = __shfl_sync(0xffffffffu, cx, wl);
+    cy = __shfl_sync(0xffffffffu, cy, wl);
+    cz = __shfl_sync(0xffffffffu, cz, wl);
+    if ((uint32_t)lane < C) {
+      const uint32_t slot = xch0 + ((par * C + rank) * NW + warp) * RS;
+      A::send(mapa(slot, lane), mapa(bar, lane), wb, widx, cx, cy, cz);
     }
 
-    // 4. combine the C records (max value, then lowest index) ------------------
+    // 3. combine the C*NW records: max value, then lowest index ---------------
     mbar_wait(bar, phase);
-    const unsigned char* recs = xch + par * kMaxCluster * RS;
-    bits_t bv;
-    int64_t bg;
-    A::recv(recs, bv, bg);
-    uint32_t rw = 0;
-    for (uint32_t r = 1; r < C; ++r) {
+    const unsigned char* recs = xch + (size_t)par * nrec * RS;
+    bits_t lv = A::bits(A::ninf());
+    uint32_t li = 0xffffffffu, lr = 0;
+    for (uint32_t r = lane; r < nrec; r += 32) {
       bits_t v;
-      int64_t g;
-      A::recv(recs + r * RS, v, g);
-      if (v > bv || (v == bv && g < bg)) {
-        bv = v;
-        bg = g;
-        rw = r;
+      uint32_t g;
+      A::recv(recs + (size_t)r * RS, v, g);
+      if (v > lv || (v == lv && g < li)) {
+        lv = v;
+        li = g;
+        lr = r;
       }
     }
-    A::recv_xyz(recs + rw * RS, px, py, pz);
+    const bits_t bv = A::warp_max(lv);
+    const uint32_t bg = __reduce_min_sync(0xffffffffu, lv == bv ? li : 0xffffffffu);
+    const int hl = __ffs(__ballot_sync(0xffffffffu, lv == bv && li == bg)) - 1;
+    const uint32_t hr = __shfl_sync(0xffffffffu, lr, hl);
+    A::recv_xyz(recs + (size_t)hr * RS, px, py, pz);
     if (rank == 0 && tid == 0) {  // fps_core.py:167-168
-      order[k] = bg;
-      sel[k] = A::from_bits(bv);
+      prm.order[b * prm.out_stride + k] = bg;
+      static_cast<T*>(prm.sel_d2)[b * prm.out_stride + k] = A::from_bits(bv);
     }
-    if (bg >= base && bg < base + Q) {  // fps_core.py:169: dist[best] = -inf
-      const int jj = (int)(bg - base);
+    const uint32_t off = bg - (uint32_t)base;
+    if (off < (uint32_t)Q) {  // fps_core.py:169: dist[best] = -inf (one owner thread)
+      const int jj = (int)off;
+      if (jj < P) {
 #pragma unroll
-      for (int j = 0; j < P; ++j)
-        if (jj == j) rd[j] = A::ninf();
+        for (int j = 0; j < P; ++j)
+          if (jj == j) {
+            if (j & 1) rd[j / 2].y = A::ninf();
+            else rd[j / 2].x = A::ninf();
+          }
+      } else if (jj < P + S) {
 #pragma unroll
-      for (int j = 0; j < S; ++j)
-        if (jj == P + j) sd[j] = A::ninf();
-      if (jj >= P + S) A::spill_store_d(spill, jj - P - S, NT, tid, A::ninf());
+        for (int j = 0; j < S; ++j)
+          if (jj == P + j) {
+            if (j & 1) sd[j / 2].y = A::ninf();
+            else sd[j / 2].x = A::ninf();
+          }
+      } else if (SPILL) {
+        A::spill_store_d(spill, jj - P - S, NT, tid, A::ninf());
+      }
     }
   }
 
   // positions -> original indices for restricted runs (fps_cache.py:197)
   if (map != nullptr && rank == 0) {
     __syncthreads();
-    for (int64_t k = tid; k < prm.iters; k += NT) order[k] = __ldg(map + order[k]);
+    int64_t* order = prm.order + b * prm.out_stride;
+    for (int k = tid; k < iters; k += NT) order[k] = __ldg(map + order[k]);
   }
   cluster_sync_all();  // no CTA leaves while peers may still push into it
 }
 
-template <typename T, int NT, int P, int S, int MINB>
+template <typename T, int NT, int P, int S, int MINB, bool SPILL = false>
 KernelInst make_inst() {
   constexpr int SG = S / Arith<T>::VW;
   KernelInst k;
@@ -424,19 +541,20 @@ KernelInst make_inst() {
   k.p = P;
   k.s = S;
   k.minb = MINB;
-  k.fn = reinterpret_cast<const void*>(&fps_greedy_kernel<T, NT, P, S, MINB>);
-  k.smem_bytes = (size_t)SG * 3 * NT * 16 + tail_bytes<T, NT>();
+  k.spill = SPILL;
+  k.fn = reinterpret_cast<const void*>(&fps_greedy_kernel<T, NT, P, S, MINB, SPILL>);
+  k.smem_base = (size_t)SG * 3 * NT * 16 + 16;
+  k.smem_per_rank = rec_bytes_per_rank<T, NT>();
   return k;
 }
 
 // Register budget: __launch_bounds__(NT, MINB) caps registers at
-// 65536 / (NT * MINB) = 128 for every instance below; per thread a register
-// slot costs 4 (f32) / 8 (f64) registers, an smem slot 1 / 2 registers plus
-// 12 / 24 bytes of shared memory.
+// 65536 / (NT * MINB) per thread; per thread a register slot costs 4 (f32) /
+// 8 (f64) registers, an smem slot 1 / 2 registers plus 12 / 24 bytes of
+// shared memory.
 const KernelInst* greedy_instances(int* count) {
   static const KernelInst insts[] = {
       // float32, 2 CTAs per SM (another cloud's CTA hides the per-iteration sync)
-      make_inst<float, 256, 1, 0, 2>(),
       make_inst<float, 256, 2, 0, 2>(),
       make_inst<float, 256, 4, 0, 2>(),
       make_inst<float, 256, 8, 0, 2>(),
@@ -444,17 +562,28 @@ const KernelInst* greedy_instances(int* count) {
       make_inst<float, 256, 16, 8, 2>(),
       make_inst<float, 256, 16, 16, 2>(),
       make_inst<float, 256, 16, 24, 2>(),
-      make_inst<float, 256, 15, 36, 2>(),
+      make_inst<float, 256, 14, 36, 2>(),
+      // float32, 3-4 CTAs per SM (smaller clouds / more clouds per SM)
+      make_inst<float, 256, 8, 20, 3>(),
+      make_inst<float, 256, 4, 16, 4>(),
+      // float32, 128-thread CTAs: fewer threads -> less per-thread overhead,
+      // more of the SM's register file + smem holds points (~25K per SM)
+      make_inst<float, 128, 28, 72, 2>(),
+      make_inst<float, 128, 10, 36, 4>(),
       // float32, 1 CTA per SM, 512 threads (largest clouds per cluster)
-      make_inst<float, 512, 15, 36, 1>(),
+      make_inst<float, 512, 14, 36, 1>(),
+      // spill variants: the rest of each thread's range streamed from HBM/L2
+      make_inst<float, 256, 14, 36, 2, true>(),
+      make_inst<float, 512, 14, 36, 1, true>(),
       // float64
-      make_inst<double, 256, 1, 0, 2>(),
       make_inst<double, 256, 2, 0, 2>(),
       make_inst<double, 256, 4, 0, 2>(),
       make_inst<double, 256, 8, 0, 2>(),
       make_inst<double, 256, 8, 8, 2>(),
-      make_inst<double, 256, 7, 18, 2>(),
-      make_inst<double, 512, 7, 18, 1>(),
+      make_inst<double, 256, 6, 18, 2>(),
+      make_inst<double, 512, 6, 18, 1>(),
+      make_inst<double, 256, 6, 18, 2, true>(),
+      make_inst<double, 512, 6, 18, 1, true>(),
   };
   *count = (int)(sizeof(insts) / sizeof(insts[0]));
   return insts;

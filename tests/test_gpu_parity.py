@@ -133,12 +133,15 @@ def test_random_batches_vs_oracle(cuda, dtype, kind):
         _check_batch(_cloud(rng, B, N, kind, dtype), m, seeds)
 
 
+# (plan "threads,register slots,smem slots,{C}", cluster sizes, has a spill variant)
 FORCED = {
-    np.float32: [("256,1,0,{C}", [1, 2, 3, 4, 7, 8, 16]), ("256,16,24,{C}", [1, 2, 5]),
-                 ("256,15,36,{C}", [1, 3, 4]), ("512,15,36,{C}", [1, 2]),
-                 ("256,8,0,{C}", [1, 16])],
-    np.float64: [("256,1,0,{C}", [1, 2, 5, 16]), ("256,8,8,{C}", [1, 3]),
-                 ("256,7,18,{C}", [1, 2, 4]), ("512,7,18,{C}", [1, 2])],
+    np.float32: [("256,2,0,{C}", [1, 2, 3, 4, 7, 8, 16], False),
+                 ("256,16,24,{C}", [1, 2, 5], False), ("256,14,36,{C}", [1, 3, 4], True),
+                 ("512,14,36,{C}", [1, 2], True), ("256,8,0,{C}", [1, 16], False),
+                 ("128,28,72,{C}", [1, 2, 4], False), ("128,10,36,{C}", [1, 3, 9], False),
+                 ("256,8,20,{C}", [2, 7], False), ("256,4,16,{C}", [1, 10], False)],
+    np.float64: [("256,2,0,{C}", [1, 2, 5, 16], False), ("256,8,8,{C}", [1, 3], False),
+                 ("256,6,18,{C}", [1, 2, 4], True), ("512,6,18,{C}", [1, 2], True)],
 }
 
 
@@ -147,12 +150,13 @@ def test_every_kernel_configuration(cuda, dtype, monkeypatch):
     """Each compiled (threads, register slots, smem slots) configuration at
     several cluster sizes, including forced spill (capacity < n)."""
     rng = np.random.default_rng(7)
-    for fmt, clusters in FORCED[dtype]:
+    for fmt, clusters, spills in FORCED[dtype]:
         for C in clusters:
             monkeypatch.setenv("FFPS_FORCE_PLAN", fmt.format(C=C))
             nt, p, s, _ = (int(v) for v in fmt.format(C=C).split(","))
             cap = nt * (p + s) * C
-            for N in sorted({max(2, cap // 3), cap, cap + 777}):   # last one spills
+            sizes = {max(2, cap // 3), cap} | ({cap + 777} if spills else set())
+            for N in sorted(sizes):
                 m = min(N, 97)
                 xyz = _cloud(rng, 2, N, "ties" if C % 2 else "uniform", dtype)
                 _check_batch(xyz, m, rng.integers(0, N, size=2))
