@@ -71,6 +71,26 @@ int ffps_run_kernel(int dtype, const void* xyz, int64_t batch,
                     int64_t map_stride, int64_t* order, void* sel_d2,
                     int64_t out_stride, void* stream);
 
+/* Greedy schedules behind ffps_run_kernel (identical results, bit for bit):
+ *   FFPS_ALGO_STREAM  K1: one thread-block cluster per cloud, every point's
+ *                     distance updated every iteration, state on chip
+ *                     (registers + shared memory), DSMEM argmax exchange —
+ *                     the "standard" exhaustive-update FPS schedule;
+ *   FFPS_ALGO_BUCKET  K0 + K1b: points binned into spatial buckets, one CTA
+ *                     per cloud; each iteration re-evaluates only the buckets
+ *                     whose exact lower bound (same rounded ops) is below
+ *                     their max distance;
+ *   FFPS_ALGO_AUTO    BUCKET for n >= 2048, else STREAM (environment variable
+ *                     FFPS_ALGO=stream|bucket overrides AUTO). */
+enum ffps_algo { FFPS_ALGO_AUTO = 0, FFPS_ALGO_STREAM = 1, FFPS_ALGO_BUCKET = 2 };
+
+/* ffps_run_kernel with an explicit schedule (same arguments; algo as above). */
+int ffps_run_kernel_ex(int dtype, const void* xyz, int64_t batch,
+                       int64_t cloud_stride, int64_t n, int64_t iters,
+                       const int64_t* seed_pos, const int64_t* index_map,
+                       int64_t map_stride, int64_t* order, void* sel_d2,
+                       int64_t out_stride, void* stream, int algo);
+
 /* Budget fill, FillMode.DETERMINISTIC_SLICE (fps_prune.py:96-100,104-105):
  * for every cloud writes order[b][k + w], w < m1 - k, = the w-th smallest
  * index of [0, n) absent from order[b][0:k), and sel_d2[b][k + w] = 0. */

@@ -16,6 +16,18 @@ from .errors import KernelError
 _DTYPE_CODE = {torch.float32: _native.F32, torch.float64: _native.F64}
 _launches = 0
 _timers: list | None = None
+_algo = "auto"
+
+
+def set_schedule(name: str) -> str:
+    """Select the greedy schedule for subsequent calls: "auto" (default),
+    "bucket" (K0+K1b, bounded re-evaluation) or "stream" (K1, every point every
+    iteration).  Results are identical; returns the previous setting."""
+    global _algo
+    if name not in _native.ALGO:
+        raise ValueError(f"unknown schedule {name!r}; expected one of {sorted(_native.ALGO)}")
+    prev, _algo = _algo, name
+    return prev
 
 
 class kernel_timer:
@@ -96,7 +108,8 @@ def greedy(xyz: torch.Tensor, n: int, iters: int, seeds: torch.Tensor,
             ev0.record(strm)
         _count(_native.run_kernel(dtype_code(xyz), xyz.data_ptr(), B, xyz.shape[1], n, iters,
                                   seeds.data_ptr(), map_ptr, map_stride, order.data_ptr(),
-                                  sel.data_ptr(), order.stride(0), _stream_handle(stream)))
+                                  sel.data_ptr(), order.stride(0), _stream_handle(stream),
+                                  _algo))
         if _timers is not None:
             ev1.record(strm)
             _timers.append((B, n, iters, ev0, ev1))

@@ -19,6 +19,7 @@ LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib",
                         "libflashfps_b200.so")
 
 F32, F64 = 0, 1
+ALGO = {"auto": 0, "stream": 1, "bucket": 2}
 _STATUS = {-1: "EINVAL", -2: "EUNSUPPORTED", -3: "ECUDA"}
 
 _lock = threading.Lock()
@@ -29,6 +30,8 @@ _i64, _vp, _int = ctypes.c_int64, ctypes.c_void_p, ctypes.c_int
 SIGNATURES = {
     "ffps_run_kernel": (_int, [_int, _vp, _i64, _i64, _i64, _i64, _vp, _vp, _i64, _vp,
                                _vp, _i64, _vp]),
+    "ffps_run_kernel_ex": (_int, [_int, _vp, _i64, _i64, _i64, _i64, _vp, _vp, _i64, _vp,
+                                  _vp, _i64, _vp, _int]),
     "ffps_fill_slice": (_int, [_int, _vp, _vp, _i64, _i64, _i64, _i64, _vp]),
     "ffps_plan": (_int, [_int, _i64, _i64, ctypes.POINTER(_i64)]),
     "ffps_last_launch_count": (_i64, []),
@@ -66,10 +69,11 @@ def check(rc: int, what: str) -> None:
 
 
 def run_kernel(dtype, xyz, batch, cloud_stride, n, iters, seed_pos, index_map, map_stride,
-               order, sel_d2, out_stride, stream) -> int:
+               order, sel_d2, out_stride, stream, algo: str = "auto") -> int:
     lib = load()
-    check(lib.ffps_run_kernel(dtype, xyz, batch, cloud_stride, n, iters, seed_pos,
-                              index_map, map_stride, order, sel_d2, out_stride, stream),
+    check(lib.ffps_run_kernel_ex(dtype, xyz, batch, cloud_stride, n, iters, seed_pos,
+                                 index_map, map_stride, order, sel_d2, out_stride, stream,
+                                 ALGO[algo]),
           "ffps_run_kernel")
     return int(lib.ffps_last_launch_count())
 

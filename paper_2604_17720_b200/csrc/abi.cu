@@ -233,33 +233,134 @@ int ffps_plan(int dtype, int64_t n, int64_t batch, int64_t* out) {
   return FFPS_OK;
 }
 
-int ffps_run_kernel(int dtype, const void* xyz, int64_t batch, int64_t cloud_stride, int64_t n,
-                    int64_t iters, const int64_t* seed_pos, const int64_t* index_map,
-                    int64_t map_stride, int64_t* order, void* sel_d2, int64_t out_stride,
-                    void* stream) {
-  g_last_launches = 0;
-  if (dtype != FFPS_F32 && dtype != FFPS_F64)
-    return fail(FFPS_EINVAL, "dtype must be FFPS_F32 or FFPS_F64");
-  if (batch < 0) return fail(FFPS_EINVAL, "batch=%lld < 0", (long long)batch);
-  if (batch == 0) return FFPS_OK;
-  if (!xyz || !seed_pos || !order || !sel_d2)
-    return fail(FFPS_EINVAL, "null device pointer");
-  if (n < 1 || n > 0x7fffffffLL) return fail(FFPS_EINVAL, "n=%lld out of range", (long long)n);
-  if (iters < 1 || iters > n)  // fps_core.py:178-180
-    return fail(FFPS_EINVAL, "m=%lld not in [1, %lld]", (long long)iters, (long long)n);
-  if (out_stride < iters) return fail(FFPS_EINVAL, "out_stride < iters");
-  if (index_map ? map_stride < n : cloud_stride < n)
-    return fail(FFPS_EINVAL, "cloud/map stride smaller than n");
-  int dev = 0;
-  cudaError_t e = cudaGetDevice(&dev);
-  if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+}  // extern "C"
+
+namespace {
+
+struct BucketPlan {
+  const ffps::BucketInst* inst = nullptr;
+  int64_t nbuckets = 0;
+  size_t smem = 0;
+};
+
+// Smallest bucket size whose bucket count fits the owned-bucket registers
+// (nt * nbt) and whose per-bucket keys fit shared memory.
+bool make_bucket_plan(int dev, int dtype, int64_t n, BucketPlan* out) {
+  const DeviceInfo di = device_info(dev);
+  int cnt = 0;
+  const ffps::BucketInst* insts = ffps::bucket_instances(&cnt);
+  const size_t static_smem = 1024;
+  for (int ppl = 1; ppl <= 4; ppl *= 2) {
+    const ffps::BucketInst* pick = nullptr;
+    const int64_t nb = (n + 32 * ppl - 1) / (32 * ppl);
+    for (int i = 0; i < cnt; ++i) {
+      const auto& k = insts[i];
+      if (k.dtype != dtype || k.ppl != ppl || (int64_t)k.nt * k.nbt < nb) continue;
+      if ((size_t)nb * k.smem_per_bucket + static_smem > di.smem_optin) continue;
+      if (!pick || k.nbt < pick->nbt) pick = &k;
+    }
+    if (pick) {
+      out->inst = pick;
+      out->nbuckets = nb;
+      out->smem = (size_t)nb * pick->smem_per_bucket;
+      return true;
+    }
+  }
+  return false;
+}
+
+int run_bucketed(int dtype, const void* xyz, int64_t batch, int64_t cloud_stride, int64_t n,
+                 int64_t iters, const int64_t* seed_pos, const int64_t* index_map,
+                 int64_t map_stride, int64_t* order, void* sel_d2, int64_t out_stride,
+                 cudaStream_t st, int dev) {
+  BucketPlan bp;
+  if (!make_bucket_plan(dev, dtype, n, &bp))
+    return fail(FFPS_EUNSUPPORTED, "no bucketed configuration for n=%lld", (long long)n);
+  const ffps::BucketInst& k = *bp.inst;
+  const int64_t bs = 32 * k.ppl;
+  const int64_t nslots = bp.nbuckets * bs;
+  const size_t esz = dtype == FFPS_F32 ? 4 : 8;
+  // scratch: X, Y, Z, D (esz) + O (4 B) per slot, boxes 6 * esz per bucket
+  const size_t per_cloud = (size_t)nslots * (4 * esz + 4) + (size_t)bp.nbuckets * 6 * esz;
+  unsigned char* scratch = nullptr;
+  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&scratch),
+                                  per_cloud * (size_t)batch + 256, st);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync(buckets)");
+  const size_t arr = (size_t)nslots * esz * (size_t)batch;
+  ffps::BucketBuildParams bb;
+  bb.xyz = xyz;
+  bb.cloud_stride = cloud_stride;
+  bb.index_map = index_map;
+  bb.map_stride = map_stride;
+  bb.n = n;
+  bb.X = scratch;
+  bb.Y = scratch + arr;
+  bb.Z = scratch + 2 * arr;
+  bb.D = scratch + 3 * arr;
+  bb.BB = scratch + 4 * arr;
+  bb.O = reinterpret_cast<int32_t*>(scratch + 4 * arr + (size_t)bp.nbuckets * 6 * esz *
+                                                            (size_t)batch);
+  bb.nslots = nslots;
+  bb.nbuckets = bp.nbuckets;
+  bb.bs = bs;
+  e = ffps::launch_bucket_build(dtype, bb, batch, st);
+  if (e != cudaSuccess) {
+    cudaFreeAsync(scratch, st);
+    return cuda_fail(e, "bucket_build_kernel launch");
+  }
+  ffps::BucketParams prm;
+  prm.X = bb.X;
+  prm.Y = bb.Y;
+  prm.Z = bb.Z;
+  prm.D = bb.D;
+  prm.O = bb.O;
+  prm.BB = bb.BB;
+  prm.nslots = nslots;
+  prm.nbuckets = bp.nbuckets;
+  prm.xyz = xyz;
+  prm.cloud_stride = cloud_stride;
+  prm.index_map = index_map;
+  prm.map_stride = map_stride;
+  prm.iters = iters;
+  prm.seed_pos = seed_pos;
+  prm.order = order;
+  prm.sel_d2 = sel_d2;
+  prm.out_stride = out_stride;
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    auto key = std::make_pair(dev, k.fn);
+    if (!g_attr_done.count(key)) {
+      e = cudaFuncSetAttribute(k.fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)(device_info_nolock(dev).smem_optin - 1024));
+      if (e != cudaSuccess) {
+        cudaFreeAsync(scratch, st);
+        return cuda_fail(e, "cudaFuncSetAttribute(bucket)");
+      }
+      g_attr_done[key] = true;
+    }
+  }
+  void* args[] = {&prm};
+  e = cudaLaunchKernel(k.fn, dim3((unsigned)batch), dim3(k.nt), args, bp.smem, st);
+  if (e != cudaSuccess) {
+    cudaFreeAsync(scratch, st);
+    return cuda_fail(e, "fps_bucket_kernel launch");
+  }
+  g_last_launches = 2;
+  e = cudaFreeAsync(scratch, st);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaFreeAsync(buckets)");
+  return FFPS_OK;
+}
+
+int run_streaming(int dtype, const void* xyz, int64_t batch, int64_t cloud_stride, int64_t n,
+                  int64_t iters, const int64_t* seed_pos, const int64_t* index_map,
+                  int64_t map_stride, int64_t* order, void* sel_d2, int64_t out_stride,
+                  cudaStream_t st, int dev) {
   Plan plan;
   if (!make_plan(dev, dtype, n, batch, &plan))
     return fail(FFPS_EUNSUPPORTED, "no kernel configuration for n=%lld", (long long)n);
   const ffps::KernelInst& k = *plan.inst;
-  e = prepare_fn(dev, k);
+  cudaError_t e = prepare_fn(dev, k);
   if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
 
   ffps::GreedyParams prm;
   prm.xyz = xyz;
@@ -309,6 +410,65 @@ int ffps_run_kernel(int dtype, const void* xyz, int64_t batch, int64_t cloud_str
     if (e != cudaSuccess) return cuda_fail(e, "cudaFreeAsync(spill)");
   }
   return FFPS_OK;
+}
+
+// FFPS_ALGO_AUTO: bucketed from kAutoBucketMin points on, streaming below
+// (tiny clouds: the cluster kernel has no bucketing pass).  FFPS_ALGO in the
+// environment ("stream" / "bucket") overrides AUTO for sweeps.
+constexpr int64_t kAutoBucketMin = 2048;
+
+int resolve_algo(int algo, int64_t n) {
+  if (algo == FFPS_ALGO_AUTO) {
+    const char* force = getenv("FFPS_FORCE_PLAN");  // names a streaming configuration
+    if (force && *force) return FFPS_ALGO_STREAM;
+    const char* env = getenv("FFPS_ALGO");
+    if (env && strcmp(env, "stream") == 0) return FFPS_ALGO_STREAM;
+    if (env && strcmp(env, "bucket") == 0) return FFPS_ALGO_BUCKET;
+    return n >= kAutoBucketMin ? FFPS_ALGO_BUCKET : FFPS_ALGO_STREAM;
+  }
+  return algo;
+}
+
+}  // namespace
+
+extern "C" {
+
+int ffps_run_kernel_ex(int dtype, const void* xyz, int64_t batch, int64_t cloud_stride,
+                       int64_t n, int64_t iters, const int64_t* seed_pos,
+                       const int64_t* index_map, int64_t map_stride, int64_t* order,
+                       void* sel_d2, int64_t out_stride, void* stream, int algo) {
+  g_last_launches = 0;
+  if (dtype != FFPS_F32 && dtype != FFPS_F64)
+    return fail(FFPS_EINVAL, "dtype must be FFPS_F32 or FFPS_F64");
+  if (algo != FFPS_ALGO_AUTO && algo != FFPS_ALGO_STREAM && algo != FFPS_ALGO_BUCKET)
+    return fail(FFPS_EINVAL, "unknown algorithm %d", algo);
+  if (batch < 0) return fail(FFPS_EINVAL, "batch=%lld < 0", (long long)batch);
+  if (batch == 0) return FFPS_OK;
+  if (!xyz || !seed_pos || !order || !sel_d2)
+    return fail(FFPS_EINVAL, "null device pointer");
+  if (n < 1 || n > 0x7fffffffLL) return fail(FFPS_EINVAL, "n=%lld out of range", (long long)n);
+  if (iters < 1 || iters > n)  // fps_core.py:178-180
+    return fail(FFPS_EINVAL, "m=%lld not in [1, %lld]", (long long)iters, (long long)n);
+  if (out_stride < iters) return fail(FFPS_EINVAL, "out_stride < iters");
+  if (index_map ? map_stride < n : cloud_stride < n)
+    return fail(FFPS_EINVAL, "cloud/map stride smaller than n");
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (resolve_algo(algo, n) == FFPS_ALGO_BUCKET)
+    return run_bucketed(dtype, xyz, batch, cloud_stride, n, iters, seed_pos, index_map,
+                        map_stride, order, sel_d2, out_stride, st, dev);
+  return run_streaming(dtype, xyz, batch, cloud_stride, n, iters, seed_pos, index_map,
+                       map_stride, order, sel_d2, out_stride, st, dev);
+}
+
+int ffps_run_kernel(int dtype, const void* xyz, int64_t batch, int64_t cloud_stride, int64_t n,
+                    int64_t iters, const int64_t* seed_pos, const int64_t* index_map,
+                    int64_t map_stride, int64_t* order, void* sel_d2, int64_t out_stride,
+                    void* stream) {
+  return ffps_run_kernel_ex(dtype, xyz, batch, cloud_stride, n, iters, seed_pos, index_map,
+                            map_stride, order, sel_d2, out_stride, stream, FFPS_ALGO_AUTO);
 }
 
 int ffps_fill_slice(int dtype, int64_t* order, void* sel_d2, int64_t batch, int64_t out_stride,

@@ -47,6 +47,55 @@ inline size_t spill_bytes_per_cta(int dtype, int nt, int g) {
   return static_cast<size_t>(g) * nt * (dtype == 0 ? 16 : 32);
 }
 
+// ---- bucketed path (K0 bucket_build.cu + K1b fps_bucket.cu) ----
+constexpr int kBucketThreads = 512;
+
+struct BucketBuildParams {
+  const void* xyz;
+  int64_t cloud_stride;
+  const int64_t* index_map;
+  int64_t map_stride;
+  int64_t n;
+  void *X, *Y, *Z, *D;  // [batch][nslots] bucket-major SoA
+  int32_t* O;           // [batch][nslots] position in the run's point list (-1: padding)
+  void* BB;             // [batch][nbuckets][6] bucket boxes
+  int64_t nslots;
+  int64_t nbuckets;
+  int64_t bs;           // points per bucket
+};
+
+struct BucketParams {
+  const void *X, *Y, *Z;
+  void* D;
+  const int32_t* O;
+  const void* BB;
+  int64_t nslots;
+  int64_t nbuckets;
+  const void* xyz;  // original input (seed coordinates)
+  int64_t cloud_stride;
+  const int64_t* index_map;
+  int64_t map_stride;
+  int64_t iters;
+  const int64_t* seed_pos;
+  int64_t* order;
+  void* sel_d2;
+  int64_t out_stride;
+};
+
+struct BucketInst {
+  int dtype;
+  int nt;
+  int ppl;  // points per lane per bucket (bucket size 32 * ppl)
+  int nbt;  // buckets owned per thread (max buckets = nt * nbt)
+  const void* fn;
+  size_t smem_per_bucket;
+};
+
+const BucketInst* bucket_instances(int* count);
+size_t bucket_build_smem();
+cudaError_t launch_bucket_build(int dtype, const BucketBuildParams& p, int64_t batch,
+                                cudaStream_t st);
+
 // K2: slice fill (fill.cu).
 cudaError_t launch_fill_slice(int dtype, int64_t* order, void* sel_d2, int64_t batch,
                               int64_t out_stride, int64_t k, int64_t m1, cudaStream_t st);

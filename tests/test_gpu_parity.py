@@ -16,8 +16,17 @@ from oracle import oracle
 pytestmark = pytest.mark.gpu
 
 
+@pytest.fixture(params=["stream", "bucket"])
+def schedule(request):
+    """Run the test under each greedy schedule (K1 streaming, K0+K1b bucketed)."""
+    from paper_2604_17720_b200 import _device
+    prev = _device.set_schedule(request.param)
+    yield request.param
+    _device.set_schedule(prev)
+
+
 # ---------------------------------------------------------------- golden (fp64)
-def test_fps_matches_reference_goldens(golden, cuda):
+def test_fps_matches_reference_goldens(golden, cuda, schedule):
     for c in golden.cases("fps"):
         cloud = ffps.PointCloud(golden.points(c))
         s, st = ffps.fps(cloud, c["m"], c["seed"])
@@ -27,7 +36,7 @@ def test_fps_matches_reference_goldens(golden, cuda):
         assert s.fill_boundary == c["m"]
 
 
-def test_fps_prune_matches_reference_goldens(golden, cuda):
+def test_fps_prune_matches_reference_goldens(golden, cuda, schedule):
     for c in golden.cases("prune"):
         cfg = ffps.PruneConfig(p=c["p"], fill_mode=ffps.FillMode(c["fill"]),
                                rng_seed=c.get("rng_seed", 0))
@@ -38,7 +47,7 @@ def test_fps_prune_matches_reference_goldens(golden, cuda):
         assert [st.distance_evals, st.iterations, st.candidates] == c["stats"]
 
 
-def test_hierarchy_matches_reference_goldens(golden, cuda):
+def test_hierarchy_matches_reference_goldens(golden, cuda, schedule):
     for c in golden.cases("hier"):
         samples, st = ffps.hierarchical_sample(ffps.PointCloud(golden.points(c)), c["budgets"],
                                                ffps.PruneConfig(p=c["p"]), c["seed"],
@@ -57,7 +66,7 @@ def test_prefix_property_goldens(golden, cuda):
         assert bool(res.ok) == c["ok"] and res.ok
 
 
-def test_fp32_goldens(golden, cuda):
+def test_fp32_goldens(golden, cuda, schedule):
     for c in golden.cases("fps32"):
         pts = torch.from_numpy(golden.points(c).astype(np.float32)).cuda()
         s, _ = ffps.fps_batch(pts, c["m"], c["seed"])
@@ -70,7 +79,7 @@ def test_fp32_goldens(golden, cuda):
 COLLINEAR = [(0, 0, 0), (1, 0, 0), (2, 0, 0), (3, 0, 0), (10, 0, 0)]
 
 
-def test_collinear_and_tiny_clouds(cuda):
+def test_collinear_and_tiny_clouds(cuda, schedule):
     s, st = ffps.fps(ffps.validate_cloud(COLLINEAR), 5, 0)
     assert s.indices.tolist() == [0, 4, 3, 1, 2]
     assert s.selection_dist2[1:].tolist() == [100.0, 9.0, 1.0, 1.0]
@@ -123,7 +132,7 @@ def _cloud(rng, B, N, kind, dtype):
 
 @pytest.mark.parametrize("dtype", [np.float32, np.float64])
 @pytest.mark.parametrize("kind", ["uniform", "ties", "grid", "collinear"])
-def test_random_batches_vs_oracle(cuda, dtype, kind):
+def test_random_batches_vs_oracle(cuda, dtype, kind, schedule):
     rng = np.random.default_rng(hash((kind, dtype().itemsize)) % 2**32)
     for N, m, B in [(1, 1, 3), (2, 2, 2), (33, 33, 2), (257, 100, 3), (1000, 250, 4),
                     (1728, 1728, 1), (5000, 1300, 3)]:
@@ -162,7 +171,7 @@ def test_every_kernel_configuration(cuda, dtype, monkeypatch):
                 _check_batch(xyz, m, rng.integers(0, N, size=2))
 
 
-def test_restricted_runs_vs_oracle(cuda):
+def test_restricted_runs_vs_oracle(cuda, schedule):
     rng = np.random.default_rng(11)
     for dtype in (np.float32, np.float64):
         xyz = _cloud(rng, 3, 3000, "ties", dtype)
@@ -170,7 +179,7 @@ def test_restricted_runs_vs_oracle(cuda):
         _check_batch(xyz, 300, np.array([0, 5, 1199]), index_map=imap)
 
 
-def test_candidate_prefix_runs_vs_oracle(cuda):
+def test_candidate_prefix_runs_vs_oracle(cuda, schedule):
     rng = np.random.default_rng(12)
     xyz = _cloud(rng, 4, 6000, "uniform", np.float32)
     _check_batch(xyz, 375, np.zeros(4, np.int64), n=1500)
@@ -178,7 +187,7 @@ def test_candidate_prefix_runs_vs_oracle(cuda):
 
 @pytest.mark.parametrize("p", [0.0, 0.25, 0.5, 0.75, 0.9])
 @pytest.mark.parametrize("cache", [True, False])
-def test_hierarchy_batch_vs_oracle(cuda, p, cache):
+def test_hierarchy_batch_vs_oracle(cuda, p, cache, schedule):
     rng = np.random.default_rng(int(p * 100) + cache)
     budgets = (1500, 375, 93, 23)
     xyz = _cloud(rng, 3, 6000, "uniform", np.float32)
@@ -250,3 +259,22 @@ def test_abi_rejects_bad_arguments(cuda):
     rc = lib.ffps_run_kernel(7, 1, 1, 10, 10, 5, 1, None, 0, 1, 1, 5, None)
     assert rc == -1
     assert lib.ffps_fill_slice(0, 1, 1, 1, 10, 5, 4, None) == -1
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+def test_bucketed_schedule_sizes_and_ties(cuda, dtype):
+    """K0+K1b forced on every size class: n below / at / above one bucket,
+    bucket sizes 32/64/128 (n up to 140K), heavy exact ties."""
+    from paper_2604_17720_b200 import _device
+    prev = _device.set_schedule("bucket")
+    try:
+        rng = np.random.default_rng(21)
+        for N, m, B, kind in [(1, 1, 2, "uniform"), (31, 31, 2, "ties"), (32, 20, 2, "grid"),
+                              (33, 33, 1, "collinear"), (1728, 900, 2, "grid"),
+                              (5000, 600, 2, "ties"), (20000, 300, 2, "uniform"),
+                              (140000, 200, 1, "ties")]:
+            if kind == "grid":
+                N = min(N, 1728)
+            _check_batch(_cloud(rng, B, N, kind, dtype), min(m, N), rng.integers(0, N, size=B))
+    finally:
+        _device.set_schedule(prev)
