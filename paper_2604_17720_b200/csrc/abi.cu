@@ -250,12 +250,15 @@ bool make_bucket_plan(int dev, int dtype, int64_t n, BucketPlan* out) {
   int cnt = 0;
   const ffps::BucketInst* insts = ffps::bucket_instances(&cnt);
   const size_t static_smem = 1024;
+  const char* want_nt = getenv("FFPS_BUCKET_NT");  // sweeps: restrict the CTA size
+  const int force_nt = want_nt ? atoi(want_nt) : 0;
   for (int ppl = 1; ppl <= 4; ppl *= 2) {
     const ffps::BucketInst* pick = nullptr;
     const int64_t nb = (n + 32 * ppl - 1) / (32 * ppl);
     for (int i = 0; i < cnt; ++i) {
       const auto& k = insts[i];
       if (k.dtype != dtype || k.ppl != ppl || (int64_t)k.nt * k.nbt < nb) continue;
+      if (force_nt && k.nt != force_nt) continue;
       if ((size_t)nb * k.smem_per_bucket + static_smem > di.smem_optin) continue;
       if (!pick || k.nbt < pick->nbt) pick = &k;
     }
@@ -326,21 +329,9 @@ int run_bucketed(int dtype, const void* xyz, int64_t batch, int64_t cloud_stride
   prm.order = order;
   prm.sel_d2 = sel_d2;
   prm.out_stride = out_stride;
-  {
-    std::lock_guard<std::mutex> lk(g_mu);
-    auto key = std::make_pair(dev, k.fn);
-    if (!g_attr_done.count(key)) {
-      e = cudaFuncSetAttribute(k.fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)(device_info_nolock(dev).smem_optin - 1024));
-      if (e != cudaSuccess) {
-        cudaFreeAsync(scratch, st);
-        return cuda_fail(e, "cudaFuncSetAttribute(bucket)");
-      }
-      g_attr_done[key] = true;
-    }
-  }
+  prm.neg_zero = -0.0f;
   void* args[] = {&prm};
-  e = cudaLaunchKernel(k.fn, dim3((unsigned)batch), dim3(k.nt), args, bp.smem, st);
+  e = cudaLaunchKernel(k.fn, dim3((unsigned)batch), dim3(k.nt), args, 0, st);
   if (e != cudaSuccess) {
     cudaFreeAsync(scratch, st);
     return cuda_fail(e, "fps_bucket_kernel launch");

@@ -84,6 +84,16 @@ struct Arith<float> {
     return __fadd_rn(__fadd_rn(__fmul_rn(gx, gx), __fmul_rn(gy, gy)), __fmul_rn(gz, gz));
   }
   static constexpr bits_t kmin = (bits_t)0x80000000;  // below every key, -inf included
+  // box_d2 with the box stored as per-axis pairs (lo, -hi) and pp = (-p, p):
+  // one FADD2 gives (RN(lo - p), RN(p - hi)) — the same two rounded values.
+  __device__ static __forceinline__ float box_d2_pairs(const float2* lnh, float2 ppx, float2 ppy,
+                                                       float2 ppz, float2 nz) {
+    const float2 ax = add2(lnh[0], ppx), ay = add2(lnh[1], ppy), az = add2(lnh[2], ppz);
+    const float2 g = make_float2(max3f(ax.x, ax.y, 0.0f), max3f(ay.x, ay.y, 0.0f));
+    const float gz = max3f(az.x, az.y, 0.0f);
+    const float2 s = sq2(g, nz);
+    return __fadd_rn(__fadd_rn(s.x, s.y), __fmul_rn(gz, gz));
+  }
   // two points at once: d = min(d, d2(p)), gm = max(gm, d.x, d.y); nz = (-0, -0)
   __device__ static __forceinline__ void upd2(pair_t& d, pair_t x, pair_t y, pair_t z,
                                               pair_t px, pair_t py, pair_t pz, pair_t nz,
@@ -161,6 +171,13 @@ struct Arith<double> {
     return __dadd_rn(__dadd_rn(__dmul_rn(gx, gx), __dmul_rn(gy, gy)), __dmul_rn(gz, gz));
   }
   static constexpr bits_t kmin = (bits_t)0x8000000000000000ull;
+  __device__ static __forceinline__ double box_d2_pairs(const double2* lnh, double2 ppx,
+                                                        double2 ppy, double2 ppz, double2) {
+    const double gx = fmax(fmax(__dadd_rn(lnh[0].x, ppx.x), __dadd_rn(lnh[0].y, ppx.y)), 0.0);
+    const double gy = fmax(fmax(__dadd_rn(lnh[1].x, ppy.x), __dadd_rn(lnh[1].y, ppy.y)), 0.0);
+    const double gz = fmax(fmax(__dadd_rn(lnh[2].x, ppz.x), __dadd_rn(lnh[2].y, ppz.y)), 0.0);
+    return __dadd_rn(__dadd_rn(__dmul_rn(gx, gx), __dmul_rn(gy, gy)), __dmul_rn(gz, gz));
+  }
   __device__ static __forceinline__ void upd2(pair_t& d, pair_t x, pair_t y, pair_t z,
                                               pair_t px, pair_t py, pair_t pz, pair_t,
                                               double& gm) {

@@ -80,6 +80,7 @@ struct BucketParams {
   int64_t* order;
   void* sel_d2;
   int64_t out_stride;
+  float neg_zero;  // -0.0f, opaque to ptxas (sq2)
 };
 
 struct BucketInst {

@@ -16,17 +16,19 @@
 // time its bucket is visited: the winner's bucket is always re-evaluated.
 //
 // State per cloud:
-//   registers  thread t owns buckets q = t + j*NT (j < NBT): box lo/hi and a
-//              cached copy of the bucket key (max distance bits, position)
-//   smem       per bucket: key value, key position, xyz of the key point;
-//              the list of buckets flagged this iteration; per-warp argmax
+//   registers  lane l of warp w owns buckets q = j*NT + l*NW + w (j < NBT):
+//              box as (lo, -hi) pairs, the bucket key (max distance bits,
+//              lowest position at that distance) and the xyz of that point
+//   smem       per-warp argmax records, double-buffered by iteration parity
 //   global/L2  X, Y, Z, D, O (bucket-major SoA, D = running min distance)
-// Per iteration: flag (bound test of owned buckets) | sync | flagged buckets
-// re-evaluated, one warp per bucket | sync | owners refresh their keys, warp
-// argmax | sync | every warp reduces the NW warp records -> next point.
+// Per iteration: packed bound test of the owned buckets -> ballot -> the warp
+// re-evaluates its own flagged buckets (32 lanes = 32 points, one L2 round
+// trip) -> owner lane refreshes the key -> warp argmax -> ONE __syncthreads
+// -> every warp reduces the NW records to the next point.
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <type_traits>
 
 #include "arith.cuh"
 #include "ffps_internal.h"
@@ -37,6 +39,7 @@ template <typename T, int NT, int PPL, int NBT>
 __global__ void __launch_bounds__(NT, 1) fps_bucket_kernel(const BucketParams prm) {
   using A = Arith<T>;
   using bits_t = typename A::bits_t;
+  using pair_t = typename A::pair_t;
   constexpr int NW = NT / 32;
   constexpr int BS = 32 * PPL;
   constexpr uint32_t kNoIdx = 0xffffffffu;
@@ -51,36 +54,35 @@ __global__ void __launch_bounds__(NT, 1) fps_bucket_kernel(const BucketParams pr
   const int32_t* __restrict__ O = prm.O + off;
   const T* __restrict__ BB = static_cast<const T*>(prm.BB) + (int64_t)b * nb * 6;
 
-  extern __shared__ __align__(16) unsigned char smem[];
-  bits_t* kv = reinterpret_cast<bits_t*>(smem);                      // [nb]
-  T* best = reinterpret_cast<T*>(smem + (size_t)nb * sizeof(bits_t)); // [nb][3]
-  uint32_t* ki = reinterpret_cast<uint32_t*>(best + (size_t)nb * 3);  // [nb]
-  int32_t* list = reinterpret_cast<int32_t*>(ki + nb);                // [nb]
-  __shared__ bits_t wv_s[NW];
-  __shared__ uint32_t wi_s[NW];
-  __shared__ int32_t wq_s[NW];
-  __shared__ int cnt;
+  // warp records, double-buffered by iteration parity: one barrier per iteration
+  __shared__ bits_t rv_s[2][NW];
+  __shared__ uint32_t ri_s[2][NW];
+  __shared__ int32_t rq_s[2][NW];
+  __shared__ T rx_s[2][NW][3];
 
-  // owned buckets: boxes in registers, keys cached (+inf => visited first)
-  T lo[NBT][3], hi[NBT][3];
+  // Owned buckets: q = j*NT + lane*NW + warp, so Morton-consecutive buckets
+  // (the ones a new point tends to hit together) belong to different warps.
+  // Box as per-axis pairs (lo, -hi); key (max distance bits, lowest position
+  // at that distance) and the xyz of that point, all in registers.
+  pair_t lnh[NBT][3];
   bits_t ov[NBT];
   uint32_t oi[NBT];
+  T ox[NBT], oy[NBT], oz[NBT];
 #pragma unroll
   for (int j = 0; j < NBT; ++j) {
-    const int q = tid + j * NT;
+    const int q = j * NT + lane * NW + warp;
     if (q < nb) {
 #pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        lo[j][c] = BB[(int64_t)q * 6 + c];
-        hi[j][c] = BB[(int64_t)q * 6 + 3 + c];
-      }
+      for (int c = 0; c < 3; ++c)
+        lnh[j][c] = A::mk(BB[(int64_t)q * 6 + c], -BB[(int64_t)q * 6 + 3 + c]);
       ov[j] = A::bits(A::pinf());
     } else {
 #pragma unroll
-      for (int c = 0; c < 3; ++c) lo[j][c] = hi[j][c] = T(0);
-      ov[j] = A::kmin;
+      for (int c = 0; c < 3; ++c) lnh[j][c] = A::mk(T(0), T(0));
+      ov[j] = A::bits(A::ninf());  // never flagged, never wins
     }
     oi[j] = kNoIdx;
+    ox[j] = oy[j] = oz[j] = T(0);
   }
 
   // seed (fps_core.py:124-130): order[0] = seed, sel[0] = +inf
@@ -98,114 +100,120 @@ __global__ void __launch_bounds__(NT, 1) fps_bucket_kernel(const BucketParams pr
   if (tid == 0) {
     order[0] = seed;
     sel[0] = A::pinf();
-    cnt = 0;
   }
   uint32_t win = (uint32_t)seed;  // position to set to -inf on its next visit
-  int prevq = -1;                 // bucket holding it (re-evaluated unconditionally)
-  __syncthreads();
+  int prevq = -1;                 // its bucket (re-evaluated unconditionally)
+  const pair_t nz = A::mk((T)prm.neg_zero, (T)prm.neg_zero);
 
   const int iters = (int)prm.iters;
   for (int k = 1; k < iters; ++k) {
-    // 1. flag owned buckets the new point can affect ------------------------------
-    uint32_t fl = 0;
+    const uint32_t par = (uint32_t)k & 1u;
+    const pair_t ppx = A::mk(-px, px), ppy = A::mk(-py, py), ppz = A::mk(-pz, pz);
+    // 1. bound test of the owned buckets ------------------------------------------
+    unsigned fm[NBT];
 #pragma unroll
     for (int j = 0; j < NBT; ++j) {
-      const int q = tid + j * NT;
-      bool f = false;
-      if (q < nb)
-        f = k == 1 || q == prevq || !(A::box_d2(px, py, pz, lo[j], hi[j]) >= A::from_bits(ov[j]));
-      const unsigned m = __ballot_sync(0xffffffffu, f);
-      if (m) {
-        const int leader = __ffs(m) - 1;
-        int pos = 0;
-        if (lane == leader) pos = atomicAdd(&cnt, __popc(m));
-        pos = __shfl_sync(0xffffffffu, pos, leader);
-        if (f) list[pos + __popc(m & ((1u << lane) - 1u))] = q;
-      }
-      fl |= (uint32_t)f << j;
+      const int q = j * NT + lane * NW + warp;
+      const T lb = A::box_d2_pairs(lnh[j], ppx, ppy, ppz, nz);
+      const bool f = !(lb >= A::from_bits(ov[j])) || q == prevq || (k == 1 && q < nb);
+      fm[j] = __ballot_sync(0xffffffffu, f);
     }
-    __syncthreads();  // A: list complete
-    const int nflag = cnt;
-
-    // 2. re-evaluate flagged buckets, one warp per bucket ---------------------------
-    for (int e = warp; e < nflag; e += NW) {
-      const int q = list[e];
-      bits_t bv = A::kmin;
-      uint32_t bi = kNoIdx;
-      T bx = T(0), by = T(0), bz = T(0);
+    // 2. the warp re-evaluates its own flagged buckets, lanes = points ------------
 #pragma unroll
-      for (int u = 0; u < PPL; ++u) {
-        const int64_t s = (int64_t)q * BS + u * 32 + lane;
-        const T x = X[s], y = Y[s], z = Z[s], d = D[s];
-        const uint32_t o = (uint32_t)O[s];
-        T nd = A::vmin(d, A::d2(x, y, z, px, py, pz));  // fps_core.py:93
-        if (o == win) nd = A::ninf();                    // fps_core.py:169
-        if (A::bits(nd) != A::bits(d)) D[s] = nd;
-        const bits_t v = A::bits(nd);
-        if (v > bv || (v == bv && o < bi)) {
-          bv = v;
-          bi = o;
-          bx = x;
-          by = y;
-          bz = z;
+    for (int j = 0; j < NBT; ++j) {
+      unsigned m = fm[j];
+      while (m) {
+        const int ol = __ffs(m) - 1;  // owner lane
+        m &= m - 1;
+        const int q = j * NT + ol * NW + warp;
+        bits_t bv = A::kmin;
+        uint32_t bi = kNoIdx;
+        T bx = T(0), by = T(0), bz = T(0);
+        T xs[PPL], ys[PPL], zs[PPL], ds[PPL];
+        uint32_t os[PPL];
+#pragma unroll
+        for (int u = 0; u < PPL; ++u) {  // all loads first (one L2 round trip)
+          const int64_t s = (int64_t)q * BS + u * 32 + lane;
+          xs[u] = X[s];
+          ys[u] = Y[s];
+          zs[u] = Z[s];
+          ds[u] = D[s];
+          os[u] = (uint32_t)O[s];
+        }
+#pragma unroll
+        for (int u = 0; u < PPL; ++u) {
+          T nd = A::vmin(ds[u], A::d2(xs[u], ys[u], zs[u], px, py, pz));  // fps_core.py:93
+          if (os[u] == win) nd = A::ninf();                               // fps_core.py:169
+          if (A::bits(nd) != A::bits(ds[u])) D[(int64_t)q * BS + u * 32 + lane] = nd;
+          const bits_t v = A::bits(nd);
+          if (v > bv || (v == bv && os[u] < bi)) {
+            bv = v;
+            bi = os[u];
+            bx = xs[u];
+            by = ys[u];
+            bz = zs[u];
+          }
+        }
+        const bits_t wv = A::warp_max(bv);
+        const uint32_t wi = __reduce_min_sync(0xffffffffu, bv == wv ? bi : kNoIdx);
+        const int wl = __ffs(__ballot_sync(0xffffffffu, bv == wv && bi == wi)) - 1;
+        bx = __shfl_sync(0xffffffffu, bx, wl);
+        by = __shfl_sync(0xffffffffu, by, wl);
+        bz = __shfl_sync(0xffffffffu, bz, wl);
+        if (lane == ol) {
+          ov[j] = wv;
+          oi[j] = wi;
+          ox[j] = bx;
+          oy[j] = by;
+          oz[j] = bz;
         }
       }
-      const bits_t wv = A::warp_max(bv);
-      const uint32_t wi = __reduce_min_sync(0xffffffffu, bv == wv ? bi : kNoIdx);
-      const int wl = __ffs(__ballot_sync(0xffffffffu, bv == wv && bi == wi)) - 1;
-      if (lane == wl) {
-        kv[q] = wv;
-        ki[q] = wi;
-        best[3 * q + 0] = bx;
-        best[3 * q + 1] = by;
-        best[3 * q + 2] = bz;
-      }
     }
-    __syncthreads();  // B: keys of re-evaluated buckets visible
-    if (tid == 0) cnt = 0;
-
-    // 3. owners refresh keys, thread / warp argmax (max value, lowest position) ---
+    // 3. thread / warp argmax over owned keys (max value, lowest position) ---------
     bits_t tv = A::kmin;
     uint32_t ti = kNoIdx;
-    int tq = -1;
+    int tj = 0;
 #pragma unroll
-    for (int j = 0; j < NBT; ++j) {
-      const int q = tid + j * NT;
-      if ((fl >> j) & 1u) {
-        ov[j] = kv[q];
-        oi[j] = ki[q];
-      }
-      if (q < nb && (ov[j] > tv || (ov[j] == tv && oi[j] < ti))) {
+    for (int j = 0; j < NBT; ++j)
+      if (ov[j] > tv || (ov[j] == tv && oi[j] < ti)) {
         tv = ov[j];
         ti = oi[j];
-        tq = q;
+        tj = j;
       }
-    }
     {
       const bits_t wv = A::warp_max(tv);
       const uint32_t wi = __reduce_min_sync(0xffffffffu, tv == wv ? ti : kNoIdx);
       const int wl = __ffs(__ballot_sync(0xffffffffu, tv == wv && ti == wi)) - 1;
       if (lane == wl) {
-        wv_s[warp] = wv;
-        wi_s[warp] = wi;
-        wq_s[warp] = tq;
+        T cx = ox[0], cy = oy[0], cz = oz[0];
+#pragma unroll
+        for (int j = 1; j < NBT; ++j)
+          if (tj == j) {
+            cx = ox[j];
+            cy = oy[j];
+            cz = oz[j];
+          }
+        rv_s[par][warp] = wv;
+        ri_s[par][warp] = wi;
+        rq_s[par][warp] = tj * NT + lane * NW + warp;
+        rx_s[par][warp][0] = cx;
+        rx_s[par][warp][1] = cy;
+        rx_s[par][warp][2] = cz;
       }
     }
-    __syncthreads();  // C: warp records visible
+    __syncthreads();  // the only barrier of the iteration
 
     // 4. every warp reduces the NW records -> the next point ------------------------
-    const bits_t rv = lane < NW ? wv_s[lane] : A::kmin;
-    const uint32_t ri = lane < NW ? wi_s[lane] : kNoIdx;
-    const int rq = lane < NW ? wq_s[lane] : -1;
+    const bits_t rv = lane < NW ? rv_s[par][lane] : A::kmin;
+    const uint32_t ri = lane < NW ? ri_s[par][lane] : kNoIdx;
     const bits_t gv = A::warp_max(rv);
     const uint32_t gi = __reduce_min_sync(0xffffffffu, rv == gv ? ri : kNoIdx);
     const int gl = __ffs(__ballot_sync(0xffffffffu, rv == gv && ri == gi)) - 1;
-    const int gq = __shfl_sync(0xffffffffu, rq, gl);
-    px = best[3 * gq + 0];
-    py = best[3 * gq + 1];
-    pz = best[3 * gq + 2];
+    px = rx_s[par][gl][0];
+    py = rx_s[par][gl][1];
+    pz = rx_s[par][gl][2];
+    prevq = rq_s[par][gl];
     win = gi;
-    prevq = gq;
     if (tid == 0) {  // fps_core.py:167-168
       order[k] = gi;
       sel[k] = A::from_bits(gv);
@@ -220,15 +228,15 @@ __global__ void __launch_bounds__(NT, 1) fps_bucket_kernel(const BucketParams pr
   }
 }
 
-template <typename T, int PPL, int NBT>
+template <typename T, int PPL, int NBT, int NT = kBucketThreads>
 BucketInst make_binst() {
   BucketInst k;
   k.dtype = sizeof(T) == 4 ? 0 : 1;
-  k.nt = kBucketThreads;
+  k.nt = NT;
   k.ppl = PPL;
   k.nbt = NBT;
-  k.fn = reinterpret_cast<const void*>(&fps_bucket_kernel<T, kBucketThreads, PPL, NBT>);
-  k.smem_per_bucket = sizeof(typename Arith<T>::bits_t) + 3 * sizeof(T) + 4 + 4;
+  k.fn = reinterpret_cast<const void*>(&fps_bucket_kernel<T, NT, PPL, NBT>);
+  k.smem_per_bucket = 0;  // bucket state lives in registers
   return k;
 }
 
@@ -236,7 +244,11 @@ const BucketInst* bucket_instances(int* count) {
   static const BucketInst insts[] = {
       make_binst<float, 1, 1>(),  make_binst<float, 1, 2>(),  make_binst<float, 1, 4>(),
       make_binst<float, 1, 8>(),  make_binst<float, 2, 4>(),  make_binst<float, 2, 8>(),
-      make_binst<float, 4, 8>(),  make_binst<double, 1, 1>(), make_binst<double, 1, 2>(),
+      make_binst<float, 4, 8>(),
+      // 256-thread variants: half the per-warp fixed overhead, twice the boxes per lane
+      make_binst<float, 1, 8, 256>(), make_binst<float, 1, 16, 256>(),
+      make_binst<float, 2, 16, 256>(),
+      make_binst<double, 1, 1>(), make_binst<double, 1, 2>(),
       make_binst<double, 1, 4>(), make_binst<double, 1, 8>(), make_binst<double, 2, 8>(),
       make_binst<double, 4, 8>(),
   };
