@@ -330,6 +330,17 @@ int run_bucketed(int dtype, const void* xyz, int64_t batch, int64_t cloud_stride
   prm.sel_d2 = sel_d2;
   prm.out_stride = out_stride;
   prm.neg_zero = -0.0f;
+  prm.trace = nullptr;
+  prm.trace_iters = 0;
+  // FFPS_TRACE_BUCKET=<device pointer>,<iterations>: phase trace of CTA 0
+  if (const char* tr = getenv("FFPS_TRACE_BUCKET")) {
+    unsigned long long ptr = 0;
+    long long it = 0;
+    if (sscanf(tr, "%llu,%lld", &ptr, &it) == 2) {
+      prm.trace = reinterpret_cast<long long*>(ptr);
+      prm.trace_iters = it;
+    }
+  }
   void* args[] = {&prm};
   e = cudaLaunchKernel(k.fn, dim3((unsigned)batch), dim3(k.nt), args, 0, st);
   if (e != cudaSuccess) {

@@ -81,6 +81,8 @@ struct BucketParams {
   void* sel_d2;
   int64_t out_stride;
   float neg_zero;  // -0.0f, opaque to ptxas (sq2)
+  long long* trace;     // optional phase trace (FFPS_TRACE_BUCKET), else null
+  int64_t trace_iters;
 };
 
 struct BucketInst {

@@ -106,8 +106,22 @@ __global__ void __launch_bounds__(NT, 1) fps_bucket_kernel(const BucketParams pr
   const pair_t nz = A::mk((T)prm.neg_zero, (T)prm.neg_zero);
 
   const int iters = (int)prm.iters;
+  // optional phase trace (tools/trace_bucket.py): CTA 0, lane 0 of every warp,
+  // per iteration {start, bound test, re-evaluation, argmax, barrier, end, flags}
+  long long* trace =
+      (prm.trace && b == 0 && lane == 0) ? prm.trace + (int64_t)warp * prm.trace_iters * 8 : nullptr;
+  // this warp's record (uniform across its lanes): best key over its buckets.
+  // Keys only decrease, so it stays valid unless its own bucket is re-evaluated.
+  bits_t rv = A::kmin;
+  uint32_t ri = kNoIdx;
+  int rq = -1;
+  T rx = T(0), ry = T(0), rz = T(0);
   for (int k = 1; k < iters; ++k) {
     const uint32_t par = (uint32_t)k & 1u;
+    long long t0 = 0, t1 = 0, t2 = 0, t3 = 0, t4 = 0;
+    int nflag_w = 0;
+    if (trace) t0 = clock64();
+    bool stale = k == 1;
     const pair_t ppx = A::mk(-px, px), ppy = A::mk(-py, py), ppz = A::mk(-pz, pz);
     // 1. bound test of the owned buckets ------------------------------------------
     unsigned fm[NBT];
@@ -117,7 +131,9 @@ __global__ void __launch_bounds__(NT, 1) fps_bucket_kernel(const BucketParams pr
       const T lb = A::box_d2_pairs(lnh[j], ppx, ppy, ppz, nz);
       const bool f = !(lb >= A::from_bits(ov[j])) || q == prevq || (k == 1 && q < nb);
       fm[j] = __ballot_sync(0xffffffffu, f);
+      nflag_w += __popc(fm[j]);
     }
+    if (trace) t1 = clock64();
     // 2. the warp re-evaluates its own flagged buckets, lanes = points ------------
 #pragma unroll
     for (int j = 0; j < NBT; ++j) {
@@ -167,41 +183,52 @@ __global__ void __launch_bounds__(NT, 1) fps_bucket_kernel(const BucketParams pr
           oy[j] = by;
           oz[j] = bz;
         }
+        stale |= (q == rq);
       }
     }
-    // 3. thread / warp argmax over owned keys (max value, lowest position) ---------
-    bits_t tv = A::kmin;
-    uint32_t ti = kNoIdx;
-    int tj = 0;
+    if (trace) t2 = clock64();
+    // 3. thread / warp argmax over owned keys (max value, lowest position), only
+    //    when the warp's record went stale --------------------------------------------
+    if (stale) {
+      bits_t tv = A::kmin;
+      uint32_t ti = kNoIdx;
+      int tj = 0;
 #pragma unroll
-    for (int j = 0; j < NBT; ++j)
-      if (ov[j] > tv || (ov[j] == tv && oi[j] < ti)) {
-        tv = ov[j];
-        ti = oi[j];
-        tj = j;
-      }
-    {
+      for (int j = 0; j < NBT; ++j)
+        if (ov[j] > tv || (ov[j] == tv && oi[j] < ti)) {
+          tv = ov[j];
+          ti = oi[j];
+          tj = j;
+        }
       const bits_t wv = A::warp_max(tv);
       const uint32_t wi = __reduce_min_sync(0xffffffffu, tv == wv ? ti : kNoIdx);
       const int wl = __ffs(__ballot_sync(0xffffffffu, tv == wv && ti == wi)) - 1;
-      if (lane == wl) {
-        T cx = ox[0], cy = oy[0], cz = oz[0];
+      T cx = ox[0], cy = oy[0], cz = oz[0];
 #pragma unroll
-        for (int j = 1; j < NBT; ++j)
-          if (tj == j) {
-            cx = ox[j];
-            cy = oy[j];
-            cz = oz[j];
-          }
-        rv_s[par][warp] = wv;
-        ri_s[par][warp] = wi;
-        rq_s[par][warp] = tj * NT + lane * NW + warp;
-        rx_s[par][warp][0] = cx;
-        rx_s[par][warp][1] = cy;
-        rx_s[par][warp][2] = cz;
-      }
+      for (int j = 1; j < NBT; ++j)
+        if (tj == j) {
+          cx = ox[j];
+          cy = oy[j];
+          cz = oz[j];
+        }
+      rv = wv;
+      ri = wi;
+      rq = __shfl_sync(0xffffffffu, tj * NT + lane * NW + warp, wl);
+      rx = __shfl_sync(0xffffffffu, cx, wl);
+      ry = __shfl_sync(0xffffffffu, cy, wl);
+      rz = __shfl_sync(0xffffffffu, cz, wl);
     }
+    if (lane == 0) {
+      rv_s[par][warp] = rv;
+      ri_s[par][warp] = ri;
+      rq_s[par][warp] = rq;
+      rx_s[par][warp][0] = rx;
+      rx_s[par][warp][1] = ry;
+      rx_s[par][warp][2] = rz;
+    }
+    if (trace) t3 = clock64();
     __syncthreads();  // the only barrier of the iteration
+    if (trace) t4 = clock64();
 
     // 4. every warp reduces the NW records -> the next point ------------------------
     const bits_t rv = lane < NW ? rv_s[par][lane] : A::kmin;
@@ -217,6 +244,10 @@ __global__ void __launch_bounds__(NT, 1) fps_bucket_kernel(const BucketParams pr
     if (tid == 0) {  // fps_core.py:167-168
       order[k] = gi;
       sel[k] = A::from_bits(gv);
+    }
+    if (trace && k < prm.trace_iters) {
+      long long* r = trace + (int64_t)k * 8;
+      r[0] = t0; r[1] = t1; r[2] = t2; r[3] = t3; r[4] = t4; r[5] = clock64(); r[6] = nflag_w;
     }
   }
 
