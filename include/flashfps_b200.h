@@ -103,6 +103,10 @@ int ffps_fill_slice(int dtype, int64_t* order, void* sel_d2, int64_t batch,
  * out[5]=resident CTAs per SM, out[6]=max resident clusters on the device. */
 int ffps_plan(int dtype, int64_t n, int64_t batch, int64_t* out);
 
+/* Bucketed-schedule configuration for n points: out[0]=threads/CTA,
+ * out[1]=points per bucket, out[2]=buckets, out[3]=buckets owned per thread. */
+int ffps_bucket_plan(int dtype, int64_t n, int64_t* out);
+
 /* Number of kernel launches the last successful call on this thread issued. */
 int64_t ffps_last_launch_count(void);
 

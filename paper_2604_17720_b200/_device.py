@@ -126,5 +126,9 @@ def fill_slice(order: torch.Tensor, sel: torch.Tensor, k: int, m1: int, stream=N
 
 
 def seeds_tensor(seed_index, B: int, device) -> torch.Tensor:
+    """(B,) int64 seed positions on ``device``, stream-ordered (no host sync
+    when every cloud starts from the same position)."""
     arr = np.broadcast_to(np.asarray(seed_index, dtype=np.int64), (B,))
+    if B > 0 and (arr == arr[0]).all():
+        return torch.full((B,), int(arr[0]), dtype=torch.int64, device=device)
     return torch.from_numpy(np.ascontiguousarray(arr)).to(device, non_blocking=False)

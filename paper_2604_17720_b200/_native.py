@@ -34,6 +34,7 @@ SIGNATURES = {
                                   _vp, _i64, _vp, _int]),
     "ffps_fill_slice": (_int, [_int, _vp, _vp, _i64, _i64, _i64, _i64, _vp]),
     "ffps_plan": (_int, [_int, _i64, _i64, ctypes.POINTER(_i64)]),
+    "ffps_bucket_plan": (_int, [_int, _i64, ctypes.POINTER(_i64)]),
     "ffps_last_launch_count": (_i64, []),
     "ffps_last_error": (ctypes.c_char_p, []),
     "ffps_abi_version": (_int, []),
@@ -91,4 +92,12 @@ def plan(dtype: int, n: int, batch: int) -> dict:
     check(lib.ffps_plan(dtype, n, batch, out), "ffps_plan")
     keys = ("threads", "reg_slots", "smem_slots", "spill_slots", "cluster",
             "ctas_per_sm", "max_clusters")
+    return dict(zip(keys, (int(v) for v in out)))
+
+
+def bucket_plan(dtype: int, n: int) -> dict:
+    lib = load()
+    out = (ctypes.c_int64 * 4)()
+    check(lib.ffps_bucket_plan(dtype, n, out), "ffps_bucket_plan")
+    keys = ("threads", "bucket_points", "buckets", "buckets_per_thread")
     return dict(zip(keys, (int(v) for v in out)))

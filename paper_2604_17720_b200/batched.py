@@ -155,9 +155,14 @@ def _fps_prune_checks(B: int, n: int, m1: int, cfg: PruneConfig, seeds: np.ndarr
     return k, c
 
 
-def _fps_prune_device(x: torch.Tensor, m1: int, cfg: PruneConfig, seeds: np.ndarray):
-    B, n = x.shape[0], x.shape[1]
+def _fps_prune_device(x: torch.Tensor, m1: int, cfg: PruneConfig, seeds: np.ndarray,
+                      n: int | None = None):
+    """``x`` holds at least the candidate prefix of every cloud; ``n`` is the
+    logical cloud size (x.shape[1] when the whole cloud is on the device)."""
+    B = x.shape[0]
+    n = x.shape[1] if n is None else n
     k, c = _fps_prune_checks(B, n, m1, cfg, seeds)
+    assert x.shape[1] >= c
     order = torch.empty((B, m1), dtype=torch.int64, device=x.device)
     sel = torch.empty((B, m1), dtype=x.dtype, device=x.device)
     # candidates are the store prefix [0, c): kernel positions == original indices
@@ -248,36 +253,78 @@ def hierarchical_sample_batch(xyz, budgets: Sequence[int], cfg: PruneConfig, see
     return layers, total, per_layer
 
 
+_STREAMS: dict = {}
+
+
+def _side_streams(dev: torch.device, n: int) -> list:
+    """Cached side streams of ``dev`` for the chunked host pipeline."""
+    have = _STREAMS.setdefault(dev.index, [])
+    while len(have) < n:
+        have.append(torch.cuda.Stream(dev))
+    return have[:n]
+
+
 def hierarchical_sample_host(points, budgets: Sequence[int], cfg: PruneConfig, seed_index=0,
-                             cache_enabled: bool = True, *, device=None, out=None):
+                             cache_enabled: bool = True, *, device=None, out=None,
+                             chunks: int = 4):
     """End-to-end call from HOST buffers: ``points`` (B, N, 3) float32/float64
     numpy array or (preferably pinned) CPU tensor.  Copies the clouds to the
     device, runs the pipeline, copies every layer's indices and selection
     distances back and synchronises.  Returns (layers, total) with layers a
     list of (indices int64 (B, M_l), selection_dist2 (B, M_l), fill_boundary)
     host tensors; ``out`` may pass preallocated pinned (indices, sel) tensors
-    of shape (B, M1) for layer 1 (deeper cache-on layers are views of it)."""
+    of shape (B, M1) for layer 1 (deeper cache-on layers are views of it).
+
+    With the cache on only the candidate prefix points[:, :c] is ever read
+    (the greedy run is on points[:c], fps_prune.py:92; the fill and the cached
+    layers are index-only), so only that prefix is copied.  The batch is split
+    into ``chunks`` groups of clouds on separate streams so the copies of one
+    group overlap the kernels of the others."""
     dev = _device.require_cuda(device)
+    b = _budgets(budgets)
+    B, N = _shape(points)
+    if b[0] > N:
+        raise BudgetExceedsCloud(f"M1={b[0]} exceeds cloud size {N}")
+    seeds = _seed_array(seed_index, B)
+    k, c = _fps_prune_checks(B, N, b[0], cfg, seeds)
     host = points if isinstance(points, torch.Tensor) else torch.from_numpy(
         np.ascontiguousarray(points))
-    x = host.to(dev, non_blocking=host.is_pinned())
-    layers, total, _ = hierarchical_sample_batch(x, budgets, cfg, seed_index, cache_enabled)
-    res = []
-    if cache_enabled:
-        l1 = layers[0]
-        if out is not None:
-            hi, hs = out
-            hi.copy_(l1.indices, non_blocking=True)
-            hs.copy_(l1.selection_dist2, non_blocking=True)
-        else:
-            hi = l1.indices.to("cpu", non_blocking=False)
-            hs = l1.selection_dist2.to("cpu", non_blocking=False)
-        for s in layers:
-            m = len(s)
-            res.append((hi[:, :m], hs[:, :m], s.fill_boundary))
+    if not cache_enabled:
+        x = host.to(dev, non_blocking=host.is_pinned())
+        layers, total, _ = hierarchical_sample_batch(x, b, cfg, seed_index, False)
+        res = [(s.indices.to("cpu", non_blocking=True),
+                s.selection_dist2.to("cpu", non_blocking=True), s.fill_boundary)
+               for s in layers]
+        torch.cuda.current_stream(dev).synchronize()
+        return res, total
+    pinned = host.is_pinned()
+    if out is not None:
+        hi, hs = out
     else:
-        for s in layers:
-            res.append((s.indices.to("cpu", non_blocking=True),
-                        s.selection_dist2.to("cpu", non_blocking=True), s.fill_boundary))
-    torch.cuda.current_stream(dev).synchronize()
+        hi = torch.empty((B, b[0]), dtype=torch.int64, pin_memory=pinned)
+        hs = torch.empty((B, b[0]), dtype=host.dtype, pin_memory=pinned)
+    nch = max(1, min(chunks, B))
+    bounds = [B * i // nch for i in range(nch + 1)]
+    main = torch.cuda.current_stream(dev)
+    streams = [main] if nch == 1 else _side_streams(dev, nch)
+    stats1 = None
+    for i, st in enumerate(streams):
+        lo, up = bounds[i], bounds[i + 1]
+        if up <= lo:
+            continue
+        if st is not main:
+            st.wait_stream(main)
+        with torch.cuda.stream(st):
+            x = host[lo:up, :c].to(dev, non_blocking=pinned)
+            l1, stats1 = _fps_prune_device(x, b[0], cfg, seeds[lo:up], n=N)
+            hi[lo:up].copy_(l1.indices, non_blocking=pinned)
+            hs[lo:up].copy_(l1.selection_dist2, non_blocking=pinned)
+    for st in streams:
+        if st is not main:
+            main.wait_stream(st)
+    main.synchronize()
+    stats1.cache_bytes = cache_footprint_bytes(b[0])
+    res = [(hi[:, :m], hs[:, :m], min(k, m)) for m in b]
+    total = SamplerStats(distance_evals=stats1.distance_evals, iterations=stats1.iterations,
+                         candidates=stats1.candidates, cache_bytes=stats1.cache_bytes)
     return res, total

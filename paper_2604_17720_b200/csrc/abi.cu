@@ -435,6 +435,22 @@ int resolve_algo(int algo, int64_t n) {
 
 extern "C" {
 
+int ffps_bucket_plan(int dtype, int64_t n, int64_t* out) {
+  if ((dtype != FFPS_F32 && dtype != FFPS_F64) || n < 1 || !out)
+    return fail(FFPS_EINVAL, "ffps_bucket_plan: bad arguments");
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+  BucketPlan bp;
+  if (!make_bucket_plan(dev, dtype, n, &bp))
+    return fail(FFPS_EUNSUPPORTED, "no bucketed configuration for n=%lld", (long long)n);
+  out[0] = bp.inst->nt;
+  out[1] = 32 * bp.inst->ppl;
+  out[2] = bp.nbuckets;
+  out[3] = bp.inst->nbt;
+  return FFPS_OK;
+}
+
 int ffps_run_kernel_ex(int dtype, const void* xyz, int64_t batch, int64_t cloud_stride,
                        int64_t n, int64_t iters, const int64_t* seed_pos,
                        const int64_t* index_map, int64_t map_stride, int64_t* order,

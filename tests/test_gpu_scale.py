@@ -115,3 +115,19 @@ def test_exhaustive_four_stage_restricted_stages_bit_exact(schedule):
         for li, (wi, ws) in enumerate(want):
             assert np.array_equal(layers[li].indices[b].cpu().numpy(), wi), (b, li)
             assert np.array_equal(layers[li].selection_dist2[b].cpu().numpy(), ws), (b, li)
+
+
+@pytest.mark.parametrize("chunks", [1, 3])
+def test_host_pipeline_matches_device_pipeline(chunks):
+    """hierarchical_sample_host (prefix-only copy, chunked streams) returns
+    exactly the device pipeline's layers."""
+    N, budgets = SHAPES["C2"]
+    xn = _uniform(7, N, 500)
+    cfg = ffps.PruneConfig(p=0.75)
+    want, tot_w, _ = ffps.hierarchical_sample_batch(torch.from_numpy(xn).cuda(), budgets, cfg)
+    got, tot_g = ffps.hierarchical_sample_host(torch.from_numpy(xn).pin_memory(), budgets, cfg,
+                                               chunks=chunks)
+    for (gi, gs, fb), w in zip(got, want):
+        assert torch.equal(gi, w.indices.cpu()) and torch.equal(gs, w.selection_dist2.cpu())
+        assert fb == w.fill_boundary
+    assert tot_g.distance_evals == tot_w.distance_evals and tot_g.cache_bytes == tot_w.cache_bytes
