@@ -97,6 +97,16 @@ int ffps_run_kernel_ex(int dtype, const void* xyz, int64_t batch,
 int ffps_fill_slice(int dtype, int64_t* order, void* sel_d2, int64_t batch,
                     int64_t out_stride, int64_t k, int64_t m1, void* stream);
 
+/* Covering radius of samples (replaces coverage_radius / _min_dist2_to,
+ * metrics.py:29-52): out_d2[b] = max over p in xyz[b][0:n) of min over
+ * i < m of d2(p, xyz[b][idx[b][i]]), the reference's rounded d2; the caller
+ * takes sqrt (metrics.py:52).  Bit-exact (max/min of exactly rounded d2).
+ *   idx     [batch][idx_stride] int64 sample indices into the cloud
+ *   out_d2  [batch] float/double (dtype) */
+int ffps_coverage(int dtype, const void* xyz, int64_t batch, int64_t cloud_stride,
+                  int64_t n, const int64_t* idx, int64_t idx_stride, int64_t m,
+                  void* out_d2, void* stream);
+
 /* Kernel configuration the library would use (for benches / reports).
  * out[0]=threads/CTA, out[1]=register slots/thread, out[2]=smem slots/thread,
  * out[3]=spill slots/thread, out[4]=CTAs per cluster (per cloud),

@@ -18,13 +18,15 @@ from .fps_cache import (BYTES_PER_ENTRY, CacheRecord, LayerBudgets, PrefixCheckR
 from .fps_core import OrderedSample, SamplerStats, fps, run_kernel
 from .fps_prune import FillMode, PruneConfig, candidate_prune, fps_prune
 from .geometry import Point3, PointCloud, squared_distance, validate_cloud
+from .metrics import coverage_d2_batch, coverage_radius, coverage_radius_batch
 
 __version__ = "0.1.0"
 
 __all__ = [
     "BYTES_PER_ENTRY", "BatchSample", "CacheRecord", "FillMode", "LayerBudgets",
     "OrderedSample", "Point3", "PointCloud", "PrefixCheckResult", "PruneConfig",
-    "SamplerStats", "cache_footprint", "candidate_prune", "errors", "fps", "fps_batch",
+    "SamplerStats", "cache_footprint", "candidate_prune", "coverage_d2_batch",
+    "coverage_radius", "coverage_radius_batch", "errors", "fps", "fps_batch",
     "fps_prune", "fps_prune_batch", "hierarchical_sample", "hierarchical_sample_batch",
     "hierarchical_sample_detailed", "hierarchical_sample_host", "prefix_reuse", "read_cache",
     "run_kernel", "run_restricted", "run_restricted_batch", "squared_distance",

@@ -132,3 +132,16 @@ def seeds_tensor(seed_index, B: int, device) -> torch.Tensor:
     if B > 0 and (arr == arr[0]).all():
         return torch.full((B,), int(arr[0]), dtype=torch.int64, device=device)
     return torch.from_numpy(np.ascontiguousarray(arr)).to(device, non_blocking=False)
+
+
+def coverage(xyz: torch.Tensor, idx: torch.Tensor, out: torch.Tensor, stream=None) -> None:
+    """K0 x2 + K5: out[b] = max_p min_s d2(p, s) over xyz[b] and xyz[b][idx[b]]."""
+    B = xyz.shape[0]
+    if B == 0:
+        return
+    assert xyz.is_cuda and xyz.is_contiguous() and idx.dtype == torch.int64
+    assert idx.stride(1) == 1 and out.dtype == xyz.dtype and out.is_contiguous()
+    with torch.cuda.device(xyz.device):
+        _count(_native.coverage(dtype_code(xyz), xyz.data_ptr(), B, xyz.shape[1], xyz.shape[1],
+                                idx.data_ptr(), idx.stride(0), idx.shape[1], out.data_ptr(),
+                                _stream_handle(stream)))

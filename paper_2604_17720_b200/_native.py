@@ -33,6 +33,7 @@ SIGNATURES = {
     "ffps_run_kernel_ex": (_int, [_int, _vp, _i64, _i64, _i64, _i64, _vp, _vp, _i64, _vp,
                                   _vp, _i64, _vp, _int]),
     "ffps_fill_slice": (_int, [_int, _vp, _vp, _i64, _i64, _i64, _i64, _vp]),
+    "ffps_coverage": (_int, [_int, _vp, _i64, _i64, _i64, _vp, _i64, _i64, _vp, _vp]),
     "ffps_plan": (_int, [_int, _i64, _i64, ctypes.POINTER(_i64)]),
     "ffps_bucket_plan": (_int, [_int, _i64, ctypes.POINTER(_i64)]),
     "ffps_last_launch_count": (_i64, []),
@@ -83,6 +84,13 @@ def fill_slice(dtype, order, sel_d2, batch, out_stride, k, m1, stream) -> int:
     lib = load()
     check(lib.ffps_fill_slice(dtype, order, sel_d2, batch, out_stride, k, m1, stream),
           "ffps_fill_slice")
+    return int(lib.ffps_last_launch_count())
+
+
+def coverage(dtype, xyz, batch, cloud_stride, n, idx, idx_stride, m, out_d2, stream) -> int:
+    lib = load()
+    check(lib.ffps_coverage(dtype, xyz, batch, cloud_stride, n, idx, idx_stride, m, out_d2,
+                            stream), "ffps_coverage")
     return int(lib.ffps_last_launch_count())
 
 

@@ -489,6 +489,98 @@ int ffps_run_kernel(int dtype, const void* xyz, int64_t batch, int64_t cloud_str
                             map_stride, order, sel_d2, out_stride, stream, FFPS_ALGO_AUTO);
 }
 
+int ffps_coverage(int dtype, const void* xyz, int64_t batch, int64_t cloud_stride, int64_t n,
+                  const int64_t* idx, int64_t idx_stride, int64_t m, void* out_d2,
+                  void* stream) {
+  g_last_launches = 0;
+  if (dtype != FFPS_F32 && dtype != FFPS_F64)
+    return fail(FFPS_EINVAL, "dtype must be FFPS_F32 or FFPS_F64");
+  if (batch < 0 || n < 1 || n > 0x7fffffffLL || m < 1 || m > 0x7fffffffLL)
+    return fail(FFPS_EINVAL, "coverage: bad sizes");
+  if (batch == 0) return FFPS_OK;
+  if (!xyz || !idx || !out_d2) return fail(FFPS_EINVAL, "null device pointer");
+  if (cloud_stride < n || idx_stride < m) return fail(FFPS_EINVAL, "stride smaller than size");
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+  const DeviceInfo di = device_info(dev);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const size_t esz = dtype == FFPS_F32 ? 4 : 8;
+  // sample buckets: boxes staged in shared memory -> bucket size from the budget
+  int64_t bss = 32;
+  while ((m + bss - 1) / bss * 6 * (int64_t)esz > (int64_t)di.smem_optin - 4096) bss *= 2;
+  const int64_t bsp = 32;
+  const int64_t nbp = (n + bsp - 1) / bsp, nbs = (m + bss - 1) / bss;
+  const int64_t nsp = nbp * bsp, nss = nbs * bss;
+  const size_t per_p = (size_t)nsp * (4 * esz + 4) + (size_t)nbp * 6 * esz;
+  const size_t per_s = (size_t)nss * (4 * esz + 4) + (size_t)nbs * 6 * esz;
+  unsigned char* scratch = nullptr;
+  e = cudaMallocAsync(reinterpret_cast<void**>(&scratch), (per_p + per_s) * (size_t)batch + 512,
+                      st);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync(coverage)");
+  auto carve = [&](unsigned char* base, int64_t nslots, int64_t nb, int64_t bs,
+                   ffps::BucketBuildParams& bb) {
+    const size_t arr = (size_t)nslots * esz * (size_t)batch;
+    bb.X = base;
+    bb.Y = base + arr;
+    bb.Z = base + 2 * arr;
+    bb.D = base + 3 * arr;
+    bb.BB = base + 4 * arr;
+    bb.O = reinterpret_cast<int32_t*>(base + 4 * arr + (size_t)nb * 6 * esz * (size_t)batch);
+    bb.nslots = nslots;
+    bb.nbuckets = nb;
+    bb.bs = bs;
+  };
+  ffps::BucketBuildParams bp{}, bs{};
+  bp.xyz = xyz;
+  bp.cloud_stride = cloud_stride;
+  bp.index_map = nullptr;
+  bp.map_stride = 0;
+  bp.n = n;
+  carve(scratch, nsp, nbp, bsp, bp);
+  bs.xyz = xyz;
+  bs.cloud_stride = cloud_stride;
+  bs.index_map = idx;
+  bs.map_stride = idx_stride;
+  bs.n = m;
+  carve(scratch + per_p * (size_t)batch, nss, nbs, bss, bs);
+  int launches = 0;
+  e = ffps::launch_bucket_build(dtype, bp, batch, st);
+  if (e == cudaSuccess) {
+    ++launches;
+    e = ffps::launch_bucket_build(dtype, bs, batch, st);
+  }
+  if (e == cudaSuccess) {
+    ++launches;
+    e = cudaMemsetAsync(out_d2, 0, (size_t)batch * esz, st);
+  }
+  if (e == cudaSuccess) {
+    ffps::CoverageParams cp;
+    cp.pX = bp.X;
+    cp.pY = bp.Y;
+    cp.pZ = bp.Z;
+    cp.pBB = bp.BB;
+    cp.p_nslots = nsp;
+    cp.p_nbuckets = nbp;
+    cp.p_bs = bsp;
+    cp.sX = bs.X;
+    cp.sY = bs.Y;
+    cp.sZ = bs.Z;
+    cp.sBB = bs.BB;
+    cp.s_nslots = nss;
+    cp.s_nbuckets = nbs;
+    cp.s_bs = bss;
+    cp.out = out_d2;
+    e = ffps::launch_coverage(dtype, cp, batch, di.sms, st);
+    if (e == cudaSuccess) ++launches;
+  }
+  cudaError_t e2 = cudaFreeAsync(scratch, st);
+  if (e != cudaSuccess) return cuda_fail(e, "coverage launch");
+  if (e2 != cudaSuccess) return cuda_fail(e2, "cudaFreeAsync(coverage)");
+  g_last_launches = launches;
+  return FFPS_OK;
+}
+
 int ffps_fill_slice(int dtype, int64_t* order, void* sel_d2, int64_t batch, int64_t out_stride,
                     int64_t k, int64_t m1, void* stream) {
   g_last_launches = 0;

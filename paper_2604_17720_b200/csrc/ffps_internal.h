@@ -99,6 +99,17 @@ size_t bucket_build_smem();
 cudaError_t launch_bucket_build(int dtype, const BucketBuildParams& p, int64_t batch,
                                 cudaStream_t st);
 
+// ---- K5 coverage radius (coverage.cu) ----
+struct CoverageParams {
+  const void *pX, *pY, *pZ, *pBB;  // cloud points, K0 buckets
+  int64_t p_nslots, p_nbuckets, p_bs;
+  const void *sX, *sY, *sZ, *sBB;  // sampled points, K0 buckets
+  int64_t s_nslots, s_nbuckets, s_bs;
+  void* out;  // [batch] max-min d2 (T), zero-initialised
+};
+cudaError_t launch_coverage(int dtype, const CoverageParams& p, int64_t batch, int sms,
+                            cudaStream_t st);
+
 // K2: slice fill (fill.cu).
 cudaError_t launch_fill_slice(int dtype, int64_t* order, void* sel_d2, int64_t batch,
                               int64_t out_stride, int64_t k, int64_t m1, cudaStream_t st);

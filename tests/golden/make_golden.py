@@ -192,6 +192,31 @@ def main():
         o, s = _run_kernel_f32_numpy(pts.astype(np.float32), m, 0)
         add({"op": "fps32", "cloud": cl, "m": m, "seed": 0}, indices=o, sel=s)
 
+    # ---- coverage radius (metrics.py:45-52) of fps / fps_prune / random samples
+    arrays["lit__line"] = np.array([(0, 0, 0), (10, 0, 0)], dtype=float)
+    add({"op": "coverage", "literal": "lit__line", "sample": "given",
+         "value": ref.coverage_radius(np.array([0]), ref.PointCloud(arrays["lit__line"]))},
+        sample=np.array([0]))
+    for t, (kind, n, m, how) in enumerate((("uniform", 50, 50, "all"),
+                                           ("uniform", 3000, 300, "fps"),
+                                           ("ties", 2000, 400, "fps"),
+                                           ("clusters", 4000, 500, "prune"),
+                                           ("uniform32", 6000, 700, "random"),
+                                           ("ties", 1500, 1, "random"),
+                                           ("uniform32", 24000, 1500, "prune"))):
+        pts, cl = cloud_entry(kind, n, 9000 + t)
+        cloud = ref.PointCloud(pts)
+        if how == "all":
+            idx = np.arange(n)
+        elif how == "fps":
+            idx = ref.fps(cloud, m, 0)[0].indices
+        elif how == "prune":
+            idx = ref.fps_prune(cloud, m, ref.PruneConfig(p=0.75), 0)[0].indices
+        else:
+            idx = np.random.default_rng(t).choice(n, size=m, replace=False)
+        add({"op": "coverage", "cloud": cl, "sample": how,
+             "value": ref.coverage_radius(idx, cloud)}, sample=idx)
+
     np.savez_compressed(os.path.join(HERE, "golden.npz"), **arrays)
     meta = {"numpy": np.__version__, "reference": "/root/reference/pkg (flashfps "
             f"{ref.__version__})", "cases": cases}
