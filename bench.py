@@ -67,12 +67,20 @@ def parse():
 def lidar_cloud(n: int, seed: int) -> np.ndarray:
     """Deterministic LiDAR-like frame (no reference generator exists):
     64 beams from -25 to +3 degrees elevation, sensor 1.8 m above a ground
-    plane, seeded box obstacles, range <= 80 m, 2 cm noise; ~1/r^2 density."""
+    plane, seeded box obstacles, range <= 80 m, 2 cm noise; ~1/r^2 density.
+    Random draws come from numpy default_rng(seed); the ray/box slab tests run
+    in torch (CUDA when available, else CPU) in float64."""
+    import torch
+    dev = "cuda" if torch.cuda.is_available() else "cpu"
     rng = np.random.default_rng(seed)
     nb = 64
     elev = np.deg2rad(np.linspace(-25.0, 3.0, nb))
     boxes = np.column_stack([rng.uniform(-60, 60, 40), rng.uniform(-60, 60, 40),
                              rng.uniform(1.0, 6.0, 40), rng.uniform(1.0, 3.5, 40)])
+    lo = torch.tensor(np.stack([boxes[:, 0] - boxes[:, 2], boxes[:, 1] - boxes[:, 2],
+                                np.full(len(boxes), -1.8)], 1), device=dev)
+    hi = torch.tensor(np.stack([boxes[:, 0] + boxes[:, 2], boxes[:, 1] + boxes[:, 2],
+                                -1.8 + boxes[:, 3]], 1), device=dev)
     out = np.empty((0, 3))
     while out.shape[0] < n:
         m = 2 * n
@@ -82,15 +90,17 @@ def lidar_cloud(n: int, seed: int) -> np.ndarray:
         r = np.full(m, 80.0)
         down = d[:, 2] < 0
         r[down] = np.minimum(80.0, 1.8 / -d[down, 2])
-        for cx, cy, half, h in boxes:   # slab test of rays from the sensor
-            lo = np.array([cx - half, cy - half, -1.8])
-            hi = np.array([cx + half, cy + half, -1.8 + h])
-            with np.errstate(divide="ignore", invalid="ignore"):
-                t1, t2 = lo / d, hi / d
-            tmin = np.max(np.minimum(t1, t2), 1)
-            tmax = np.min(np.maximum(t1, t2), 1)
+        dt = torch.tensor(d, device=dev)
+        rt = torch.tensor(r, device=dev)
+        for c0 in range(0, m, 1 << 16):   # slab test of every ray against every box
+            iv = (1.0 / dt[c0:c0 + (1 << 16)])[:, None, :]
+            t1, t2 = lo[None] * iv, hi[None] * iv
+            tmin = torch.nan_to_num(torch.minimum(t1, t2), nan=-torch.inf).amax(2)
+            tmax = torch.nan_to_num(torch.maximum(t1, t2), nan=torch.inf).amin(2)
             hit = (tmax >= tmin) & (tmin > 0)
-            r = np.where(hit, np.minimum(r, tmin), r)
+            th = torch.where(hit, tmin, torch.full_like(tmin, torch.inf)).amin(1)
+            rt[c0:c0 + (1 << 16)] = torch.minimum(rt[c0:c0 + (1 << 16)], th)
+        r = rt.cpu().numpy()
         keep = r < 80.0
         p = d[keep] * r[keep, None] + rng.normal(0, 0.02, (int(keep.sum()), 3))
         out = np.vstack([out, p])
@@ -383,6 +393,25 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                      "ms_per_step": fs_step, "schedule": "stream (K1)",
                      "speedup_flash_stream_vs_standard_exhaustive": sd_step / fs_step}
 
+    # matched sampling-quality metric (north star): covering radius of layer 1
+    # (metrics.py:45-52) for FlashFPS vs the exhaustive run, every cloud
+    quality = None
+    if not args.no_exhaustive:
+        fl_l, _, _ = ffps.hierarchical_sample_batch(x, budgets, cfg_flash, 0, True)
+        ex_l, _, _ = ffps.hierarchical_sample_batch(x, budgets, cfg_exh, 0, False)
+        torch.cuda.synchronize()
+        qs, qe = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        qs.record()
+        r_fl = ffps.coverage_radius_batch(x, fl_l[0].indices)
+        qe.record()
+        r_ex = ffps.coverage_radius_batch(x, ex_l[0].indices)
+        torch.cuda.synchronize()
+        ratio = (r_fl / r_ex).cpu().numpy()
+        quality = {"metric": "coverage radius of layer 1 (k-center objective, metrics.py:45-52)",
+                   "flash_mean": float(r_fl.mean()), "exhaustive_mean": float(r_ex.mean()),
+                   "ratio_median": float(np.median(ratio)), "ratio_max": float(ratio.max()),
+                   "coverage_kernel_ms_per_batch": qs.elapsed_time(qe), "clouds": B}
+
     # roofline of the dominant kernel (K1 on the flash stage)
     c1, k1 = stage_units(args.n, budgets, args.p, True)[0]
     units_launch = B * c1 * (k1 - 1)
@@ -442,6 +471,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                       "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
               "gpu_launches": launches, "roofline": roof, "exhaustive": exh,
               "exhaustive_standard": exh_std, "flash_standard_schedule": flash_std,
+              "quality": quality,
               "cpu_baseline": cpu, "clocks": clocks,
               "step_ms": [round(v, 4) for v in ms]})
 
