@@ -419,7 +419,8 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     pk = peaks()
     achieved = units_launch * BYTES_PER_UNIT_F32 / (kms / 1e3) / 1e9
     plan = {"schedule": "bucket", **_native.bucket_plan(_native.F32, c1)} \
-        if c1 >= 2048 else {"schedule": "stream", **_native.plan(_native.F32, c1, B)}
+        if c1 >= 2048 and (B >= 48 or c1 >= 150000) else \
+        {"schedule": "stream", **_native.plan(_native.F32, c1, B)}
     sm_mhz = clocks["sm_mhz"] or pk["sm_max_mhz"]
     issue_ceiling = 148 * 128 * sm_mhz * 1e6 / 9.0   # ~9 FP32-pipe instr / unit
     traffic = None

@@ -80,8 +80,9 @@ int ffps_run_kernel(int dtype, const void* xyz, int64_t batch,
  *                     per cloud; each iteration re-evaluates only the buckets
  *                     whose exact lower bound (same rounded ops) is below
  *                     their max distance;
- *   FFPS_ALGO_AUTO    BUCKET for n >= 2048, else STREAM (environment variable
- *                     FFPS_ALGO=stream|bucket overrides AUTO). */
+ *   FFPS_ALGO_AUTO    BUCKET when n >= 2048 and (batch >= 48 or n >= 150000),
+ *                     else STREAM (environment variable FFPS_ALGO=stream|bucket
+ *                     overrides AUTO). */
 enum ffps_algo { FFPS_ALGO_AUTO = 0, FFPS_ALGO_STREAM = 1, FFPS_ALGO_BUCKET = 2 };
 
 /* ffps_run_kernel with an explicit schedule (same arguments; algo as above). */

@@ -252,6 +252,7 @@ bool make_bucket_plan(int dev, int dtype, int64_t n, BucketPlan* out) {
   const size_t static_smem = 1024;
   const char* want_nt = getenv("FFPS_BUCKET_NT");  // sweeps: restrict the CTA size
   const int force_nt = want_nt ? atoi(want_nt) : 0;
+
   for (int ppl = 1; ppl <= 4; ppl *= 2) {
     const ffps::BucketInst* pick = nullptr;
     const int64_t nb = (n + 32 * ppl - 1) / (32 * ppl);
@@ -283,8 +284,9 @@ int run_bucketed(int dtype, const void* xyz, int64_t batch, int64_t cloud_stride
   const int64_t bs = 32 * k.ppl;
   const int64_t nslots = bp.nbuckets * bs;
   const size_t esz = dtype == FFPS_F32 ? 4 : 8;
-  // scratch: X, Y, Z, D (esz) + O (4 B) per slot, boxes 6 * esz per bucket
-  const size_t per_cloud = (size_t)nslots * (4 * esz + 4) + (size_t)bp.nbuckets * 6 * esz;
+  // scratch: X, Y, Z, D (esz) + O (4 B) per slot, boxes 6 * esz per bucket,
+  // + TX, TY, TZ, TO for the second sort level of K0
+  const size_t per_cloud = (size_t)nslots * (7 * esz + 8) + (size_t)bp.nbuckets * 6 * esz;
   unsigned char* scratch = nullptr;
   cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&scratch),
                                   per_cloud * (size_t)batch + 256, st);
@@ -306,6 +308,17 @@ int run_bucketed(int dtype, const void* xyz, int64_t batch, int64_t cloud_stride
   bb.nslots = nslots;
   bb.nbuckets = bp.nbuckets;
   bb.bs = bs;
+  const char* sort2 = getenv("FFPS_BUCKET_SORT2");  // "0": single-level binning (sweeps)
+  if (sort2 && strcmp(sort2, "0") == 0) {
+    bb.TX = bb.TY = bb.TZ = nullptr;
+    bb.TO = nullptr;
+  } else {
+    unsigned char* t = reinterpret_cast<unsigned char*>(bb.O) + (size_t)nslots * 4 * (size_t)batch;
+    bb.TX = t;
+    bb.TY = t + arr;
+    bb.TZ = t + 2 * arr;
+    bb.TO = reinterpret_cast<int32_t*>(t + 3 * arr);
+  }
   e = ffps::launch_bucket_build(dtype, bb, batch, st);
   if (e != cudaSuccess) {
     cudaFreeAsync(scratch, st);
@@ -414,19 +427,26 @@ int run_streaming(int dtype, const void* xyz, int64_t batch, int64_t cloud_strid
   return FFPS_OK;
 }
 
-// FFPS_ALGO_AUTO: bucketed from kAutoBucketMin points on, streaming below
-// (tiny clouds: the cluster kernel has no bucketing pass).  FFPS_ALGO in the
+// FFPS_ALGO_AUTO (measured on B200, tools/bench_configs.py): the bucketed
+// schedule runs one CTA per cloud and wins when the batch alone fills the GPU
+// (>= 48 clouds) or the clouds are so large that the streaming schedule runs
+// in several waves / spills (>= 150K points); below that the streaming
+// schedule spreads each cloud over many SMs and wins.  FFPS_ALGO in the
 // environment ("stream" / "bucket") overrides AUTO for sweeps.
 constexpr int64_t kAutoBucketMin = 2048;
+constexpr int64_t kAutoBucketBatch = 48;
+constexpr int64_t kAutoBucketLarge = 150000;
 
-int resolve_algo(int algo, int64_t n) {
+int resolve_algo(int algo, int64_t n, int64_t batch) {
   if (algo == FFPS_ALGO_AUTO) {
     const char* force = getenv("FFPS_FORCE_PLAN");  // names a streaming configuration
     if (force && *force) return FFPS_ALGO_STREAM;
     const char* env = getenv("FFPS_ALGO");
     if (env && strcmp(env, "stream") == 0) return FFPS_ALGO_STREAM;
     if (env && strcmp(env, "bucket") == 0) return FFPS_ALGO_BUCKET;
-    return n >= kAutoBucketMin ? FFPS_ALGO_BUCKET : FFPS_ALGO_STREAM;
+    return n >= kAutoBucketMin && (batch >= kAutoBucketBatch || n >= kAutoBucketLarge)
+               ? FFPS_ALGO_BUCKET
+               : FFPS_ALGO_STREAM;
   }
   return algo;
 }
@@ -474,7 +494,7 @@ int ffps_run_kernel_ex(int dtype, const void* xyz, int64_t batch, int64_t cloud_
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if (resolve_algo(algo, n) == FFPS_ALGO_BUCKET)
+  if (resolve_algo(algo, n, batch) == FFPS_ALGO_BUCKET)
     return run_bucketed(dtype, xyz, batch, cloud_stride, n, iters, seed_pos, index_map,
                         map_stride, order, sel_d2, out_stride, st, dev);
   return run_streaming(dtype, xyz, batch, cloud_stride, n, iters, seed_pos, index_map,
@@ -530,6 +550,8 @@ int ffps_coverage(int dtype, const void* xyz, int64_t batch, int64_t cloud_strid
     bb.nslots = nslots;
     bb.nbuckets = nb;
     bb.bs = bs;
+    bb.TX = bb.TY = bb.TZ = nullptr;
+    bb.TO = nullptr;
   };
   ffps::BucketBuildParams bp{}, bs{};
   bp.xyz = xyz;

@@ -26,6 +26,9 @@ namespace ffps {
 constexpr int kBuildThreads = 1024;
 constexpr int kGridBits = 5;                          // 32 cells per axis
 constexpr int kCells = 1 << (3 * kGridBits);          // 32768 cells
+constexpr int kSubBits = 3;                           // 8^3 sub-cells in a crowded cell
+constexpr int kSub = 1 << (3 * kSubBits);
+constexpr int kCrowd = 64;                            // cells above this are refined
 
 __device__ __forceinline__ uint32_t spread3(uint32_t v) {  // 5 bits -> every 3rd bit
   uint32_t r = 0;
@@ -197,6 +200,95 @@ __global__ void __launch_bounds__(kBuildThreads, 1) bucket_build_kernel(const Bu
   }
   __syncthreads();  // global writes of the block visible to the block
 
+  // 4b. second level: inside every crowded cell (> kCrowd points; skewed
+  //     densities such as LiDAR frames) order the points by the Morton code of
+  //     an 8^3 grid over the cell's own box.  One warp per cell, per-warp
+  //     histogram in shared memory, scatter through the T* scratch arrays.
+  if (p.TX != nullptr) {
+    uint32_t* sub = hist + kCells + warp * kSub;  // [kSub] per warp
+    T* TX = static_cast<T*>(p.TX) + base;
+    T* TY = static_cast<T*>(p.TY) + base;
+    T* TZ = static_cast<T*>(p.TZ) + base;
+    int32_t* TO = p.TO + base;
+    for (int c = warp; c < kCells; c += kBuildThreads / 32) {
+      const int beg = c == 0 ? 0 : (int)hist[c - 1];
+      const int end = (int)hist[c];
+      if (end - beg <= kCrowd) continue;
+      T a[3] = {pinf, pinf, pinf}, zz[3] = {-pinf, -pinf, -pinf};
+      for (int i = beg + lane; i < end; i += 32) {
+        const T v[3] = {X[i], Y[i], Z[i]};
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+          a[d] = v[d] < a[d] ? v[d] : a[d];
+          zz[d] = v[d] > zz[d] ? v[d] : zz[d];
+        }
+      }
+      T sinv[3];
+#pragma unroll
+      for (int d = 0; d < 3; ++d) {
+        a[d] = warp_min(a[d]);
+        zz[d] = warp_maxv(zz[d]);
+        const T ext = zz[d] - a[d];
+        sinv[d] = ext > (T)0 ? (T)(1 << kSubBits) / ext : (T)0;
+      }
+      auto scell = [&](T x, T y, T z) -> uint32_t {
+        auto cc = [&](T v, int d) {
+          int q = (int)((v - a[d]) * sinv[d]);
+          return (uint32_t)(q < 0 ? 0 : (q >= (1 << kSubBits) ? (1 << kSubBits) - 1 : q));
+        };
+        uint32_t r = 0;
+#pragma unroll
+        for (int i = 0; i < kSubBits; ++i)
+          r |= (((cc(x, 0) >> i) & 1u) << (3 * i)) | (((cc(y, 1) >> i) & 1u) << (3 * i + 1)) |
+               (((cc(z, 2) >> i) & 1u) << (3 * i + 2));
+        return r;
+      };
+      for (int i = lane; i < kSub; i += 32) sub[i] = 0;
+      __syncwarp();
+      for (int i = beg + lane; i < end; i += 32) atomicAdd(&sub[scell(X[i], Y[i], Z[i])], 1u);
+      __syncwarp();
+      // exclusive scan of the kSub counters (kSub / 32 per lane)
+      constexpr int kPerLane = kSub / 32;
+      uint32_t loc[kPerLane], sum = 0;
+#pragma unroll
+      for (int j = 0; j < kPerLane; ++j) {
+        loc[j] = sub[lane * kPerLane + j];
+        sum += loc[j];
+      }
+      uint32_t incl = sum;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t u = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += u;
+      }
+      uint32_t run = (uint32_t)beg + incl - sum;
+#pragma unroll
+      for (int j = 0; j < kPerLane; ++j) {
+        sub[lane * kPerLane + j] = run;
+        run += loc[j];
+      }
+      __syncwarp();
+      for (int i = beg + lane; i < end; i += 32) {
+        const T x = X[i], y = Y[i], z = Z[i];
+        const int32_t o = O[i];
+        const uint32_t s = atomicAdd(&sub[scell(x, y, z)], 1u);
+        TX[s] = x;
+        TY[s] = y;
+        TZ[s] = z;
+        TO[s] = o;
+      }
+      __syncwarp();
+      for (int i = beg + lane; i < end; i += 32) {
+        X[i] = TX[i];
+        Y[i] = TY[i];
+        Z[i] = TZ[i];
+        O[i] = TO[i];
+      }
+      __syncwarp();
+    }
+    __syncthreads();
+  }
+
   // 5. padding of the last bucket
   const int first_last = (int)((p.nbuckets - 1) * p.bs);
   for (int s = n + tid; s < (int)p.nslots; s += kBuildThreads) {
@@ -235,7 +327,9 @@ __global__ void __launch_bounds__(kBuildThreads, 1) bucket_build_kernel(const Bu
   }
 }
 
-size_t bucket_build_smem() { return (size_t)kCells * sizeof(uint32_t); }
+size_t bucket_build_smem() {
+  return (size_t)(kCells + (kBuildThreads / 32) * kSub) * sizeof(uint32_t);
+}
 
 cudaError_t launch_bucket_build(int dtype, const BucketBuildParams& p, int64_t batch,
                                 cudaStream_t st) {

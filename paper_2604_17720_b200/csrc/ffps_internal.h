@@ -62,6 +62,8 @@ struct BucketBuildParams {
   int64_t nslots;
   int64_t nbuckets;
   int64_t bs;           // points per bucket
+  void *TX, *TY, *TZ;   // [batch][nslots] scratch for the second sort level (or null)
+  int32_t* TO;
 };
 
 struct BucketParams {

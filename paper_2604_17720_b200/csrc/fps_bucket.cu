@@ -259,6 +259,7 @@ __global__ void __launch_bounds__(NT, 1) fps_bucket_kernel(const BucketParams pr
   }
 }
 
+
 template <typename T, int PPL, int NBT, int NT = kBucketThreads>
 BucketInst make_binst() {
   BucketInst k;

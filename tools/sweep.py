@@ -52,6 +52,9 @@ def main():
     g = torch.Generator(device="cuda").manual_seed(0)
     x = torch.rand((a.batch, N, 3), generator=g, device="cuda", dtype=torch.float64).to(dt)
     units = a.batch * a.n * (a.iters - 1)
+    import subprocess
+    clk = subprocess.run(["nvidia-smi", "--query-gpu=clocks.sm,clocks.max.sm,power.draw,temperature.gpu",
+                          "--format=csv,noheader"], capture_output=True, text=True).stdout.strip()
     ref = None
     for plan in [""] + a.plans:
         os.environ["FFPS_FORCE_PLAN"] = plan
@@ -65,7 +68,7 @@ def main():
         same = bool(torch.equal(order, ref))
         info = _native.plan(_native.F32 if dt == torch.float32 else _native.F64, a.n, a.batch) \
             if not plan else {}
-        print(json.dumps({"plan": plan or "auto", "ms": round(ms, 4),
+        print(json.dumps({"plan": plan or "auto", "ms": round(ms, 4), "idle_clk": clk,
                           "ns_per_iter": round(ms * 1e6 / a.iters, 1),
                           "gunits_per_s": round(units / ms / 1e6, 1), "same_as_auto": same,
                           **({"auto": info} if info else {})}), flush=True)
