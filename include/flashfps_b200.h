@@ -85,6 +85,19 @@ int ffps_run_kernel(int dtype, const void* xyz, int64_t batch,
  *                     overrides AUTO). */
 enum ffps_algo { FFPS_ALGO_AUTO = 0, FFPS_ALGO_STREAM = 1, FFPS_ALGO_BUCKET = 2 };
 
+/* Host -> device copy of the candidate prefix xyz[b][0:n_prefix) of every
+ * cloud (the only coordinates a cache-on FlashFPS run reads,
+ * fps_prune.py:92) into a dense [batch][n_prefix][3] device buffer: one
+ * pitched copy (source pitch = cloud_stride points).  `src_host` should be
+ * pinned for the copy to be asynchronous. */
+int ffps_h2d_prefix(void* dst, const void* src_host, int64_t batch, int64_t n_prefix,
+                    int64_t cloud_stride, int dtype, void* stream);
+
+/* The schedule FFPS_ALGO_AUTO picks for a batch of `batch` clouds of n points
+ * (FFPS_ALGO_STREAM or FFPS_ALGO_BUCKET); callers that split one batch into
+ * chunks decide once for the whole batch. */
+int ffps_auto_schedule(int64_t n, int64_t batch);
+
 /* ffps_run_kernel with an explicit schedule (same arguments; algo as above). */
 int ffps_run_kernel_ex(int dtype, const void* xyz, int64_t batch,
                        int64_t cloud_stride, int64_t n, int64_t iters,

@@ -19,6 +19,10 @@ _timers: list | None = None
 _algo = "auto"
 
 
+def current_schedule() -> str:
+    return _algo
+
+
 def set_schedule(name: str) -> str:
     """Select the greedy schedule for subsequent calls: "auto" (default),
     "bucket" (K0+K1b, bounded re-evaluation) or "stream" (K1, every point every

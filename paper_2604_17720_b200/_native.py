@@ -36,6 +36,8 @@ SIGNATURES = {
     "ffps_coverage": (_int, [_int, _vp, _i64, _i64, _i64, _vp, _i64, _i64, _vp, _vp]),
     "ffps_plan": (_int, [_int, _i64, _i64, ctypes.POINTER(_i64)]),
     "ffps_bucket_plan": (_int, [_int, _i64, ctypes.POINTER(_i64)]),
+    "ffps_auto_schedule": (_int, [_i64, _i64]),
+    "ffps_h2d_prefix": (_int, [_vp, _vp, _i64, _i64, _i64, _int, _vp]),
     "ffps_last_launch_count": (_i64, []),
     "ffps_last_error": (ctypes.c_char_p, []),
     "ffps_abi_version": (_int, []),
@@ -109,3 +111,13 @@ def bucket_plan(dtype: int, n: int) -> dict:
     check(lib.ffps_bucket_plan(dtype, n, out), "ffps_bucket_plan")
     keys = ("threads", "bucket_points", "buckets", "buckets_per_thread")
     return dict(zip(keys, (int(v) for v in out)))
+
+
+def auto_schedule(n: int, batch: int) -> str:
+    """The schedule AUTO picks for a whole batch ("stream" or "bucket")."""
+    return {1: "stream", 2: "bucket"}[int(load().ffps_auto_schedule(n, batch))]
+
+
+def h2d_prefix(dst, src_host, batch, n_prefix, cloud_stride, dtype, stream) -> None:
+    check(load().ffps_h2d_prefix(dst, src_host, batch, n_prefix, cloud_stride, dtype, stream),
+          "ffps_h2d_prefix")

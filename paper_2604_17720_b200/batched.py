@@ -305,23 +305,40 @@ def hierarchical_sample_host(points, budgets: Sequence[int], cfg: PruneConfig, s
         hs = torch.empty((B, b[0]), dtype=host.dtype, pin_memory=pinned)
     nch = max(1, min(chunks, B))
     bounds = [B * i // nch for i in range(nch + 1)]
-    main = torch.cuda.current_stream(dev)
-    streams = [main] if nch == 1 else _side_streams(dev, nch)
-    stats1 = None
-    for i, st in enumerate(streams):
-        lo, up = bounds[i], bounds[i + 1]
-        if up <= lo:
-            continue
-        if st is not main:
-            st.wait_stream(main)
-        with torch.cuda.stream(st):
-            x = host[lo:up, :c].to(dev, non_blocking=pinned)
-            l1, stats1 = _fps_prune_device(x, b[0], cfg, seeds[lo:up], n=N)
-            hi[lo:up].copy_(l1.indices, non_blocking=pinned)
-            hs[lo:up].copy_(l1.selection_dist2, non_blocking=pinned)
-    for st in streams:
-        if st is not main:
-            main.wait_stream(st)
+    # one schedule for the whole batch (AUTO would otherwise decide per chunk)
+    from . import _native
+    sched = _device.current_schedule()
+    if sched == "auto":
+        sched = _native.auto_schedule(c, B)
+    prev = _device.set_schedule(sched)
+    try:
+        main = torch.cuda.current_stream(dev)
+        streams = [main] if nch == 1 else _side_streams(dev, nch)
+        stats1 = None
+        for i, st in enumerate(streams):
+            lo, up = bounds[i], bounds[i + 1]
+            if up <= lo:
+                continue
+            if st is not main:
+                st.wait_stream(main)
+            with torch.cuda.stream(st):
+                if host.is_contiguous() and host.dtype in (torch.float32, torch.float64):
+                    # one pitched copy of the candidate prefixes (no host staging)
+                    x = torch.empty((up - lo, c, 3), dtype=host.dtype, device=dev)
+                    _native.h2d_prefix(x.data_ptr(), host[lo:up].data_ptr(), up - lo, c, N,
+                                       _device.dtype_code(x), st.cuda_stream)
+                    if not pinned:
+                        st.synchronize()  # pageable source: the copy is staged, keep it alive
+                else:
+                    x = host[lo:up, :c].to(dev, non_blocking=pinned)
+                l1, stats1 = _fps_prune_device(x, b[0], cfg, seeds[lo:up], n=N)
+                hi[lo:up].copy_(l1.indices, non_blocking=pinned)
+                hs[lo:up].copy_(l1.selection_dist2, non_blocking=pinned)
+        for st in streams:
+            if st is not main:
+                main.wait_stream(st)
+    finally:
+        _device.set_schedule(prev)
     main.synchronize()
     stats1.cache_bytes = cache_footprint_bytes(b[0])
     res = [(hi[:, :m], hs[:, :m], min(k, m)) for m in b]

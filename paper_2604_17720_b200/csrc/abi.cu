@@ -48,6 +48,20 @@ std::map<std::pair<int, const void*>, bool> g_attr_done;
 DeviceInfo device_info_nolock(int dev) {
   auto it = g_dev.find(dev);
   if (it != g_dev.end()) return it->second;
+  // Scratch (spill buffers, K0 buckets) comes from the device's default
+  // stream-ordered pool.  Its release threshold defaults to 0, i.e. the pool
+  // hands memory back at every synchronisation and the next call re-maps it
+  // on the host (tens of ms for ~100 MB); keep it.
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t keep = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    // no hidden cross-stream waits: chunks of one batch on side streams must
+    // not be serialised by the pool reusing another stream's freed block
+    int no = 0;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolReuseAllowInternalDependencies, &no);
+  }
+  cudaGetLastError();
   DeviceInfo d;
   int v = 0;
   cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
@@ -469,6 +483,27 @@ int ffps_bucket_plan(int dtype, int64_t n, int64_t* out) {
   out[2] = bp.nbuckets;
   out[3] = bp.inst->nbt;
   return FFPS_OK;
+}
+
+int ffps_h2d_prefix(void* dst, const void* src_host, int64_t batch, int64_t n_prefix,
+                    int64_t cloud_stride, int dtype, void* stream) {
+  g_last_launches = 0;
+  if ((dtype != FFPS_F32 && dtype != FFPS_F64) || batch < 0 || n_prefix < 0 ||
+      cloud_stride < n_prefix)
+    return fail(FFPS_EINVAL, "h2d_prefix: bad arguments");
+  if (batch == 0 || n_prefix == 0) return FFPS_OK;
+  if (!dst || !src_host) return fail(FFPS_EINVAL, "null pointer");
+  const size_t esz = dtype == FFPS_F32 ? 4 : 8;
+  cudaError_t e = cudaMemcpy2DAsync(dst, (size_t)n_prefix * 3 * esz, src_host,
+                                    (size_t)cloud_stride * 3 * esz, (size_t)n_prefix * 3 * esz,
+                                    (size_t)batch, cudaMemcpyHostToDevice,
+                                    static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpy2DAsync");
+  return FFPS_OK;
+}
+
+int ffps_auto_schedule(int64_t n, int64_t batch) {
+  return resolve_algo(FFPS_ALGO_AUTO, n, batch);
 }
 
 int ffps_run_kernel_ex(int dtype, const void* xyz, int64_t batch, int64_t cloud_stride,
