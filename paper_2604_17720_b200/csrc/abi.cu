@@ -275,7 +275,10 @@ bool make_bucket_plan(int dev, int dtype, int64_t n, BucketPlan* out) {
       if (k.dtype != dtype || k.ppl != ppl || (int64_t)k.nt * k.nbt < nb) continue;
       if (force_nt && k.nt != force_nt) continue;
       if ((size_t)nb * k.smem_per_bucket + static_smem > di.smem_optin) continue;
-      if (!pick || k.nbt < pick->nbt) pick = &k;
+      // default CTA size first (FFPS_BUCKET_NT selects others), then fewest boxes/lane
+      const int want = force_nt ? force_nt : ffps::kBucketThreads;
+      const bool pk = pick && pick->nt == want, kk = k.nt == want;
+      if (!pick || (kk && !pk) || (kk == pk && k.nbt < pick->nbt)) pick = &k;
     }
     if (pick) {
       out->inst = pick;
