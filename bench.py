@@ -172,6 +172,16 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------- helpers
+# Test-only switch: every rank on cuda:0 with gloo collectives, to exercise the
+# multi-rank path (barriers, max-over-ranks timing, index gather) on a 1-GPU box.
+# The ranks' kernels never wait on each other; the numbers it prints are not a
+# scaling measurement.
+SHARE_GPU = os.environ.get("FFPS_BENCH_SHARE_GPU") == "1"
+
+
+def gpu_index(local_rank: int) -> int:
+    return 0 if SHARE_GPU else local_rank
+
 def peaks() -> dict:
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
@@ -266,8 +276,8 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     from paper_2604_17720_b200 import _device, _native
     from paper_2604_17720_b200.sharded import gather_rows
 
-    torch.cuda.set_device(local_rank)
-    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(gpu_index(local_rank))
+    dev = torch.device("cuda", gpu_index(local_rank))
     _native.load()
     budgets = BUDGETS[args.n]
     B = args.batch
@@ -325,13 +335,14 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                 kern.extend(kt.kernel_ms())
         launches = _device.launches() - l0
         barrier()
-        tot = torch.tensor([sum(ms)], dtype=torch.float64, device=dev)
+        tot = torch.tensor([sum(ms)], dtype=torch.float64, device="cpu" if SHARE_GPU else dev)
         if world > 1:
             dist.all_reduce(tot, op=dist.ReduceOp.MAX)
         return float(tot.item()), ms, kern, launches
 
     vis = os.environ.get("CUDA_VISIBLE_DEVICES", "")
-    phys = vis.split(",")[local_rank] if vis and vis.split(",")[0].isdigit() else str(local_rank)
+    phys = vis.split(",")[gpu_index(local_rank)] if vis and vis.split(",")[0].isdigit() \
+        else str(gpu_index(local_rank))
     ramp()
     with ClockSampler(int(phys)) as clk:
         tot_ms, ms, kern, launches = timed(cfg_flash, True, args.steps, args.warmup, timer=True)
@@ -357,7 +368,8 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         e.record()
         torch.cuda.synchronize()
         e2e_ms.append(s.elapsed_time(e))
-    e2e_tot = torch.tensor([sum(e2e_ms)], dtype=torch.float64, device=dev)
+    e2e_tot = torch.tensor([sum(e2e_ms)], dtype=torch.float64,
+                           device="cpu" if SHARE_GPU else dev)
     if world > 1:
         dist.all_reduce(e2e_tot, op=dist.ReduceOp.MAX)
     e2e_step = float(e2e_tot.item()) / args.steps
@@ -497,8 +509,11 @@ def main():
     if world > 1:
         import torch
         import torch.distributed as dist
-        torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        torch.cuda.set_device(gpu_index(local_rank))
+        if SHARE_GPU:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     try:
         run_ours(args, rank, world, local_rank)
     finally:

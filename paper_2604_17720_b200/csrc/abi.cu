@@ -408,6 +408,16 @@ int run_streaming(int dtype, const void* xyz, int64_t batch, int64_t cloud_strid
   prm.spill = nullptr;
   prm.spill_slots = plan.G;
   prm.neg_zero = -0.0f;
+  prm.trace = nullptr;
+  prm.trace_iters = 0;
+  if (const char* tr = getenv("FFPS_TRACE_STREAM")) {  // <device pointer>,<iterations>
+    unsigned long long ptr = 0;
+    long long it = 0;
+    if (sscanf(tr, "%llu,%lld", &ptr, &it) == 2) {
+      prm.trace = reinterpret_cast<long long*>(ptr);
+      prm.trace_iters = it;
+    }
+  }
   if (plan.G > 0) {
     const size_t bytes =
         ffps::spill_bytes_per_cta(dtype, k.nt, plan.G) * (size_t)plan.C * (size_t)batch;

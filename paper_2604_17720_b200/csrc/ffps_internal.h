@@ -23,6 +23,8 @@ struct GreedyParams {
   void* spill;      // [batch][C][G][2?][NT] vectors, only when spill_slots > 0
   int spill_slots;  // G: per-thread slots streamed from global memory
   float neg_zero;   // -0.0f, opaque to ptxas (see sq2 in fps_greedy.cu)
+  long long* trace;     // optional phase trace (FFPS_TRACE_STREAM), else null
+  int64_t trace_iters;
 };
 
 // One compiled configuration of the greedy kernel.

@@ -280,8 +280,6 @@ const BucketInst* bucket_instances(int* count) {
       // 256-thread variants: half the per-warp fixed overhead, twice the boxes per lane
       make_binst<float, 1, 8, 256>(), make_binst<float, 1, 16, 256>(),
       make_binst<float, 2, 16, 256>(),
-      // 1024-thread variants: flagged buckets spread over 32 warps
-      make_binst<float, 1, 2, 1024>(), make_binst<float, 2, 4, 1024>(),
       make_binst<double, 1, 1>(), make_binst<double, 1, 2>(),
       make_binst<double, 1, 4>(), make_binst<double, 1, 8>(), make_binst<double, 2, 8>(),
       make_binst<double, 4, 8>(),

@@ -172,7 +172,14 @@ __global__ void __launch_bounds__(NT, MINB) fps_greedy_kernel(const GreedyParams
 
   const uint32_t xch0 = smem_u32(xch);
   const uint32_t nrec = C * NW;
+  // optional phase trace (FFPS_TRACE_STREAM): cluster 0, lane 0 of every warp of
+  // every rank: {start, update done, record pushed, records arrived, end}
+  long long* trace = (prm.trace && b == 0 && lane == 0)
+                         ? prm.trace + ((int64_t)rank * NW + warp) * prm.trace_iters * 8
+                         : nullptr;
   for (int k = 1; k < iters; ++k) {
+    long long t0 = 0, t1 = 0, t2 = 0, t3 = 0;
+    if (trace) t0 = clock64();
     const uint32_t par = (uint32_t)((k - 1) & 1);
     const uint32_t phase = (uint32_t)(((k - 1) >> 1) & 1);
     const uint32_t bar = mbar0 + 8 * par;
@@ -214,6 +221,7 @@ __global__ void __launch_bounds__(NT, MINB) fps_greedy_kernel(const GreedyParams
 #pragma unroll
     for (int g = 0; g < NG; ++g) tm = A::vmax(tm, gm[g]);
     const bits_t tb = A::bits(tm);
+    if (trace) t1 = clock64();
 
     // 2. warp max, lowest lane holding it finds its lowest slot ---------------
     const bits_t wb = A::warp_max(tb);
@@ -291,7 +299,9 @@ __global__ void __launch_bounds__(NT, MINB) fps_greedy_kernel(const GreedyParams
     }
 
     // 3. combine the C*NW records: max value, then lowest index ---------------
+    if (trace) t2 = clock64();
     mbar_wait(bar, phase);
+    if (trace) t3 = clock64();
     const unsigned char* recs = xch + (size_t)par * nrec * RS;
     bits_t lv = A::bits(A::ninf());
     uint32_t li = 0xffffffffu, lr = 0;
@@ -334,6 +344,10 @@ __global__ void __launch_bounds__(NT, MINB) fps_greedy_kernel(const GreedyParams
       } else if (SPILL) {
         A::spill_store_d(spill, jj - P - S, NT, tid, A::ninf());
       }
+    }
+    if (trace && k < prm.trace_iters) {
+      long long* r = trace + (int64_t)k * 8;
+      r[0] = t0; r[1] = t1; r[2] = t2; r[3] = t3; r[4] = clock64();
     }
   }
 

@@ -51,9 +51,11 @@ def gather_rows(local: torch.Tensor, batch: int, group=None) -> torch.Tensor:
                           device=local.device)
         dist.all_gather_into_tensor(out, pad, group=group)
         parts = list(out.split(rows)) if rows else [out] * world
-    else:
-        parts = [torch.empty_like(pad) for _ in range(world)]
-        dist.all_gather(parts, pad, group=group)
+    else:  # gloo: host tensors
+        host = pad.cpu()
+        parts = [torch.empty_like(host) for _ in range(world)]
+        dist.all_gather(parts, host, group=group)
+        parts = [p.to(local.device) for p in parts]
     keep = []
     for r in range(world):
         lo, hi = shard_range(batch, world, r)
