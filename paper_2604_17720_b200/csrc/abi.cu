@@ -259,10 +259,11 @@ struct BucketPlan {
 
 // Smallest bucket size whose bucket count fits the owned-bucket registers
 // (nt * nbt) and whose per-bucket keys fit shared memory.
-bool make_bucket_plan(int dev, int dtype, int64_t n, BucketPlan* out) {
+bool make_bucket_plan(int dev, int dtype, int64_t n, BucketPlan* out, bool multi = false) {
   const DeviceInfo di = device_info(dev);
   int cnt = 0;
-  const ffps::BucketInst* insts = ffps::bucket_instances(&cnt);
+  const ffps::BucketInst* insts =
+      multi ? ffps::multi_instances(&cnt) : ffps::bucket_instances(&cnt);
   const size_t static_smem = 1024;
   const char* want_nt = getenv("FFPS_BUCKET_NT");  // sweeps: restrict the CTA size
   const int force_nt = want_nt ? atoi(want_nt) : 0;
@@ -293,9 +294,9 @@ bool make_bucket_plan(int dev, int dtype, int64_t n, BucketPlan* out) {
 int run_bucketed(int dtype, const void* xyz, int64_t batch, int64_t cloud_stride, int64_t n,
                  int64_t iters, const int64_t* seed_pos, const int64_t* index_map,
                  int64_t map_stride, int64_t* order, void* sel_d2, int64_t out_stride,
-                 cudaStream_t st, int dev) {
+                 cudaStream_t st, int dev, bool multi) {
   BucketPlan bp;
-  if (!make_bucket_plan(dev, dtype, n, &bp))
+  if (!make_bucket_plan(dev, dtype, n, &bp, multi))
     return fail(FFPS_EUNSUPPORTED, "no bucketed configuration for n=%lld", (long long)n);
   const ffps::BucketInst& k = *bp.inst;
   const int64_t bs = 32 * k.ppl;
@@ -363,7 +364,7 @@ int run_bucketed(int dtype, const void* xyz, int64_t batch, int64_t cloud_stride
   prm.trace = nullptr;
   prm.trace_iters = 0;
   // FFPS_TRACE_BUCKET=<device pointer>,<iterations>: phase trace of CTA 0
-  if (const char* tr = getenv("FFPS_TRACE_BUCKET")) {
+  if (const char* tr = getenv(multi ? "FFPS_TRACE_MULTI" : "FFPS_TRACE_BUCKET")) {
     unsigned long long ptr = 0;
     long long it = 0;
     if (sscanf(tr, "%llu,%lld", &ptr, &it) == 2) {
@@ -471,6 +472,7 @@ int resolve_algo(int algo, int64_t n, int64_t batch) {
     const char* env = getenv("FFPS_ALGO");
     if (env && strcmp(env, "stream") == 0) return FFPS_ALGO_STREAM;
     if (env && strcmp(env, "bucket") == 0) return FFPS_ALGO_BUCKET;
+    if (env && strcmp(env, "multi") == 0) return FFPS_ALGO_MULTI;
     return n >= kAutoBucketMin && (batch >= kAutoBucketBatch || n >= kAutoBucketLarge)
                ? FFPS_ALGO_BUCKET
                : FFPS_ALGO_STREAM;
@@ -526,7 +528,8 @@ int ffps_run_kernel_ex(int dtype, const void* xyz, int64_t batch, int64_t cloud_
   g_last_launches = 0;
   if (dtype != FFPS_F32 && dtype != FFPS_F64)
     return fail(FFPS_EINVAL, "dtype must be FFPS_F32 or FFPS_F64");
-  if (algo != FFPS_ALGO_AUTO && algo != FFPS_ALGO_STREAM && algo != FFPS_ALGO_BUCKET)
+  if (algo != FFPS_ALGO_AUTO && algo != FFPS_ALGO_STREAM && algo != FFPS_ALGO_BUCKET &&
+      algo != FFPS_ALGO_MULTI)
     return fail(FFPS_EINVAL, "unknown algorithm %d", algo);
   if (batch < 0) return fail(FFPS_EINVAL, "batch=%lld < 0", (long long)batch);
   if (batch == 0) return FFPS_OK;
@@ -542,9 +545,10 @@ int ffps_run_kernel_ex(int dtype, const void* xyz, int64_t batch, int64_t cloud_
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if (resolve_algo(algo, n, batch) == FFPS_ALGO_BUCKET)
+  const int a = resolve_algo(algo, n, batch);
+  if (a == FFPS_ALGO_BUCKET || a == FFPS_ALGO_MULTI)
     return run_bucketed(dtype, xyz, batch, cloud_stride, n, iters, seed_pos, index_map,
-                        map_stride, order, sel_d2, out_stride, st, dev);
+                        map_stride, order, sel_d2, out_stride, st, dev, a == FFPS_ALGO_MULTI);
   return run_streaming(dtype, xyz, batch, cloud_stride, n, iters, seed_pos, index_map,
                        map_stride, order, sel_d2, out_stride, st, dev);
 }

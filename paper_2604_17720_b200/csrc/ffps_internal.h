@@ -99,6 +99,7 @@ struct BucketInst {
 };
 
 const BucketInst* bucket_instances(int* count);
+const BucketInst* multi_instances(int* count);  // K1m (fps_multi.cu)
 size_t bucket_build_smem();
 cudaError_t launch_bucket_build(int dtype, const BucketBuildParams& p, int64_t batch,
                                 cudaStream_t st);

@@ -16,7 +16,7 @@ from oracle import oracle
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(params=["stream", "bucket"])
+@pytest.fixture(params=["stream", "bucket", "multi"])
 def schedule(request):
     """Run the test under each greedy schedule (K1 streaming, K0+K1b bucketed)."""
     from paper_2604_17720_b200 import _device
@@ -261,12 +261,13 @@ def test_abi_rejects_bad_arguments(cuda):
     assert lib.ffps_fill_slice(0, 1, 1, 1, 10, 5, 4, None) == -1
 
 
+@pytest.mark.parametrize("sched", ["bucket", "multi"])
 @pytest.mark.parametrize("dtype", [np.float32, np.float64])
-def test_bucketed_schedule_sizes_and_ties(cuda, dtype):
-    """K0+K1b forced on every size class: n below / at / above one bucket,
-    bucket sizes 32/64/128 (n up to 140K), heavy exact ties."""
+def test_bucketed_schedule_sizes_and_ties(cuda, dtype, sched):
+    """K0+K1b / K0+K1m forced on every size class: n below / at / above one
+    bucket, bucket sizes 32/64/128 (n up to 140K), heavy exact ties."""
     from paper_2604_17720_b200 import _device
-    prev = _device.set_schedule("bucket")
+    prev = _device.set_schedule(sched)
     try:
         rng = np.random.default_rng(21)
         for N, m, B, kind in [(1, 1, 2, "uniform"), (31, 31, 2, "ties"), (32, 20, 2, "grid"),
