@@ -22,17 +22,19 @@
 // A round:
 //   1. bound test of every owned bucket against the J points of the previous
 //      round (box_d2 with the reference's rounded ops, as in K1b) -> ballot;
-//   2. the warp re-evaluates its flagged buckets against all J points (one L2
-//      round trip per bucket): new key (value, position, xyz) and second
-//      best v2 into the owner lane's registers; the points themselves -> -inf;
-//   3. per-warp top-KM of the owned keys (KM warp argmax steps) -> smem;
-//   | barrier |
-//   4. warp 0 merges the NW x KM records to the global top-KM, tests (a) and
-//      (b) for all candidate pairs at once, writes the accepted prefix;
-//   | barrier |
+//   2. the warp re-evaluates its flagged buckets against all J points, up to
+//      4 buckets per batch so their L2 round trips overlap: new key (value,
+//      position, xyz) and second best v2 into the owner lane's registers; the
+//      selected points themselves -> -inf;
+//   3. warp maxima -> | barrier | -> tau = smallest warp maximum; every owned
+//      key >= tau joins a candidate list (each of the NW >= KM warps holds one,
+//      so the global top-KM is in it) -> | barrier |
+//   4. warp 0 selects the top-KM of the list, tests (a) and (b) for all pairs
+//      at once, writes the accepted prefix -> | barrier |
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <type_traits>
 
 #include "arith.cuh"
 #include "ffps_internal.h"
@@ -55,8 +57,8 @@ __global__ void __launch_bounds__(NT, 1) fps_multi_kernel(const BucketParams prm
   constexpr int NW = NT / 32;
   constexpr int BS = 32 * PPL;
   constexpr uint32_t kNoIdx = 0xffffffffu;
-  constexpr int NREC = NW * KM;          // records merged by warp 0
-  constexpr int RPL = (NREC + 31) / 32;  // records per lane in the merge
+  constexpr int NREC = 128;              // capacity of the candidate list
+  constexpr int RPL = NREC / 32;         // list entries per lane in the merge
   static_assert(KM <= 32, "one candidate per lane in the chain test");
 
   const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -69,7 +71,12 @@ __global__ void __launch_bounds__(NT, 1) fps_multi_kernel(const BucketParams prm
   const int32_t* __restrict__ O = prm.O + off;
   const T* __restrict__ BB = static_cast<const T*>(prm.BB) + (int64_t)b * nb * 6;
 
-  // per-warp top-KM records and the accepted points of the round
+  // candidate list (keys >= tau), warp maxima, flagged-bucket lists and the
+  // accepted points of the round
+  __shared__ bits_t wm_s[NW];
+  __shared__ int32_t wl_s[NW][32 * NBT];
+  __shared__ uint32_t wm2_s[NW][32 * NBT];  // points (of the J) flagging each listed bucket
+  __shared__ int ncand_s;
   __shared__ bits_t rv_s[NREC], r2_s[NREC];
   __shared__ uint32_t ri_s[NREC];
   __shared__ int32_t rq_s[NREC];
@@ -128,9 +135,10 @@ __global__ void __launch_bounds__(NT, 1) fps_multi_kernel(const BucketParams prm
     long long t0 = 0, t1 = 0, t2 = 0, t3 = 0, t4 = 0;
     if (trace) t0 = clock64();
     // 1. bound test against the J points of the last round ----------------------
-    unsigned fm[NBT];
+    unsigned fm[NBT];  // warp ballot: bucket flagged
+    unsigned pm[NBT];  // lane: which of the J points flag its bucket
 #pragma unroll
-    for (int j = 0; j < NBT; ++j) fm[j] = 0u;
+    for (int j = 0; j < NBT; ++j) pm[j] = 0u;
     for (int t = 0; t < J; ++t) {
       const T px = sp_s[t][0], py = sp_s[t][1], pz = sp_s[t][2];
       const int sq = sq_s[t];
@@ -140,54 +148,78 @@ __global__ void __launch_bounds__(NT, 1) fps_multi_kernel(const BucketParams prm
         const int q = j * NT + lane * NW + warp;
         const T lb = A::box_d2_pairs(lnh[j], ppx, ppy, ppz, nz);
         const bool f = q < nb && (round == 0 || q == sq || !(lb >= A::from_bits(ov[j])));
-        fm[j] |= __ballot_sync(0xffffffffu, f);
+        pm[j] |= (unsigned)f << t;
       }
     }
+#pragma unroll
+    for (int j = 0; j < NBT; ++j) fm[j] = __ballot_sync(0xffffffffu, pm[j] != 0u);
     if (trace) t1 = clock64();
-    // 2. re-evaluate the flagged buckets against all J points ----------------------
+    // 2. re-evaluate the flagged buckets against all J points: compacted per-warp
+    //    list, up to 4 buckets per batch so their L2 round trips overlap ---------
+    int nf = 0;
 #pragma unroll
     for (int j = 0; j < NBT; ++j) {
-      unsigned m = fm[j];
-      while (m) {
-        const int ol = __ffs(m) - 1;
-        m &= m - 1u;
-        const int q = j * NT + ol * NW + warp;
-        T xs[PPL], ys[PPL], zs[PPL], ds[PPL], d0[PPL];
-        uint32_t os[PPL];
+      if ((fm[j] >> lane) & 1u) {
+        const int e = nf + __popc(fm[j] & ((1u << lane) - 1u));
+        wl_s[warp][e] = j * NT + lane * NW + warp;
+        wm2_s[warp][e] = pm[j];
+      }
+      nf += __popc(fm[j]);
+    }
+    __syncwarp();
+    auto batch = [&](auto chn, int e0) {
+      constexpr int CH = decltype(chn)::value;
+      int qc[CH];
+      T xs[CH][PPL], ys[CH][PPL], zs[CH][PPL], ds[CH][PPL], d0[CH][PPL];
+      uint32_t os[CH][PPL];
+#pragma unroll
+      for (int c = 0; c < CH; ++c) {
+        qc[c] = wl_s[warp][e0 + c];
 #pragma unroll
         for (int u = 0; u < PPL; ++u) {
-          const int64_t s = (int64_t)q * BS + u * 32 + lane;
-          xs[u] = X[s];
-          ys[u] = Y[s];
-          zs[u] = Z[s];
-          ds[u] = D[s];
-          os[u] = (uint32_t)O[s];
-          d0[u] = ds[u];
+          const int64_t s = (int64_t)qc[c] * BS + u * 32 + lane;
+          xs[c][u] = X[s];
+          ys[c][u] = Y[s];
+          zs[c][u] = Z[s];
+          ds[c][u] = D[s];
+          os[c][u] = (uint32_t)O[s];
+          d0[c][u] = ds[c][u];
         }
-        for (int t = 0; t < J; ++t) {
+      }
+      // only the points that flagged a bucket can change it (bound argument)
+#pragma unroll
+      for (int c = 0; c < CH; ++c) {
+        unsigned pmask = wm2_s[warp][e0 + c];
+        while (pmask) {
+          const int t = __ffs(pmask) - 1;
+          pmask &= pmask - 1u;
           const T px = sp_s[t][0], py = sp_s[t][1], pz = sp_s[t][2];
           const uint32_t pw = si_s[t];
 #pragma unroll
           for (int u = 0; u < PPL; ++u) {
-            T nd = A::vmin(ds[u], A::d2(xs[u], ys[u], zs[u], px, py, pz));  // :93
-            if (os[u] == pw) nd = A::ninf();                                // :169
-            ds[u] = nd;
+            T nd = A::vmin(ds[c][u], A::d2(xs[c][u], ys[c][u], zs[c][u], px, py, pz));  // :93
+            if (os[c][u] == pw) nd = A::ninf();                                          // :169
+            ds[c][u] = nd;
           }
         }
+      }
+#pragma unroll
+      for (int c = 0; c < CH; ++c) {
+        const int q = qc[c];
         bits_t b1 = A::kmin, b2 = A::kmin;
         uint32_t i1 = kNoIdx;
         T x1 = T(0), y1 = T(0), z1 = T(0);
 #pragma unroll
         for (int u = 0; u < PPL; ++u) {
-          if (A::bits(ds[u]) != A::bits(d0[u])) D[(int64_t)q * BS + u * 32 + lane] = ds[u];
-          const bits_t v = A::bits(ds[u]);
-          if (v > b1 || (v == b1 && os[u] < i1)) {
+          if (A::bits(ds[c][u]) != A::bits(d0[c][u])) D[(int64_t)q * BS + u * 32 + lane] = ds[c][u];
+          const bits_t v = A::bits(ds[c][u]);
+          if (v > b1 || (v == b1 && os[c][u] < i1)) {
             b2 = b1;
             b1 = v;
-            i1 = os[u];
-            x1 = xs[u];
-            y1 = ys[u];
-            z1 = zs[u];
+            i1 = os[c][u];
+            x1 = xs[c][u];
+            y1 = ys[c][u];
+            z1 = zs[c][u];
           } else if (v > b2) {
             b2 = v;
           }
@@ -199,67 +231,125 @@ __global__ void __launch_bounds__(NT, 1) fps_multi_kernel(const BucketParams prm
         x1 = __shfl_sync(0xffffffffu, x1, wl);
         y1 = __shfl_sync(0xffffffffu, y1, wl);
         z1 = __shfl_sync(0xffffffffu, z1, wl);
+        const int jq = q / NT, ol = (q % NT) / NW;
         if (lane == ol) {
-          ov[j] = wv;
-          oi[j] = wi;
-          o2[j] = w2;
-          ox[j] = x1;
-          oy[j] = y1;
-          oz[j] = z1;
+#pragma unroll
+          for (int j = 0; j < NBT; ++j)
+            if (j == jq) {
+              ov[j] = wv;
+              oi[j] = wi;
+              o2[j] = w2;
+              ox[j] = x1;
+              oy[j] = y1;
+              oz[j] = z1;
+            }
         }
       }
+    };
+    constexpr int MAXCH = PPL >= 4 ? 1 : 4 / PPL;  // <= 4 points per lane in flight
+    for (int e0 = 0; e0 < nf; e0 += MAXCH) {
+      const int r = nf - e0;
+      if (r >= MAXCH) batch(std::integral_constant<int, MAXCH>{}, e0);
+      else if (MAXCH > 2 && r == 3) batch(std::integral_constant<int, (MAXCH > 2 ? 3 : 1)>{}, e0);
+      else if (MAXCH > 1 && r == 2) batch(std::integral_constant<int, (MAXCH > 1 ? 2 : 1)>{}, e0);
+      else batch(std::integral_constant<int, 1>{}, e0);
     }
     if (trace) t2 = clock64();
-    // 3. per-warp top-KM of the owned keys ------------------------------------------
+    // 3. candidates: every owned key >= tau, tau = the smallest warp maximum (each
+    //    of the NW >= KM warps holds a key >= tau, so the global top-KM is among
+    //    them) ------------------------------------------------------------------------
     {
-      unsigned taken = 0;
-#pragma unroll 1
-      for (int r = 0; r < KM; ++r) {
-        bits_t bv = A::kmin;
-        uint32_t bi = kNoIdx;
-        int bj = 0;
+      bits_t tv = A::kmin;
 #pragma unroll
-        for (int j = 0; j < NBT; ++j)
-          if (!((taken >> j) & 1u) && (ov[j] > bv || (ov[j] == bv && oi[j] < bi))) {
-            bv = ov[j];
-            bi = oi[j];
-            bj = j;
+      for (int j = 0; j < NBT; ++j) tv = ov[j] > tv ? ov[j] : tv;
+      const bits_t wv = A::warp_max(tv);
+      if (lane == 0) wm_s[warp] = wv;
+      if (tid == 0) ncand_s = 0;
+    }
+    if (trace) t3 = clock64();
+    __syncthreads();  // B1: warp maxima visible, list empty
+    {
+      const bits_t wv = lane < NW ? wm_s[lane] : A::bits(A::pinf());
+      const bits_t tau = -A::warp_max(-wv);  // min over the NW warp maxima
+#pragma unroll
+      for (int j = 0; j < NBT; ++j) {
+        const bool c = ov[j] >= tau && ov[j] != A::kmin;
+        const unsigned m = __ballot_sync(0xffffffffu, c);
+        if (m) {
+          int base = 0;
+          if (lane == 0) base = atomicAdd(&ncand_s, __popc(m));
+          base = __shfl_sync(0xffffffffu, base, 0);
+          const int e = base + __popc(m & ((1u << lane) - 1u));
+          if (c && e < NREC) {
+            rv_s[e] = ov[j];
+            ri_s[e] = oi[j];
+            r2_s[e] = o2[j];
+            rq_s[e] = j * NT + lane * NW + warp;
+            rx_s[e][0] = ox[j];
+            rx_s[e][1] = oy[j];
+            rx_s[e][2] = oz[j];
           }
-        const int wl = argmax_lane<A>(bv, bi);
-        if (lane == wl) {
-          taken |= 1u << bj;
-          const int e = warp * KM + r;
-          rv_s[e] = bv;
-          ri_s[e] = bi;
-          T cx = ox[0], cy = oy[0], cz = oz[0];
-          bits_t c2 = o2[0];
-#pragma unroll
-          for (int j = 1; j < NBT; ++j)
-            if (bj == j) {
-              cx = ox[j];
-              cy = oy[j];
-              cz = oz[j];
-              c2 = o2[j];
-            }
-          r2_s[e] = c2;
-          rq_s[e] = bj * NT + lane * NW + warp;
-          rx_s[e][0] = cx;
-          rx_s[e][1] = cy;
-          rx_s[e][2] = cz;
         }
       }
     }
-    if (trace) t3 = clock64();
-    __syncthreads();  // B1: records visible
+    __syncthreads();  // B2: candidate list complete
     // 4. warp 0: global top-KM, chain test, accepted prefix ------------------------
-    if (warp == 0) {
+    const int ncand = ncand_s;
+    if (ncand > NREC) {
+      // more than NREC keys at or above tau (massive ties, exhausted buckets):
+      // take just the exact argmax this round (one more barrier, CTA-uniform)
+      bits_t tv = A::kmin;
+      uint32_t ti = kNoIdx;
+      int tj = 0;
+#pragma unroll
+      for (int j = 0; j < NBT; ++j)
+        if (ov[j] > tv || (ov[j] == tv && oi[j] < ti)) {
+          tv = ov[j];
+          ti = oi[j];
+          tj = j;
+        }
+      T cx = ox[0], cy = oy[0], cz = oz[0];
+#pragma unroll
+      for (int j = 1; j < NBT; ++j)
+        if (tj == j) {
+          cx = ox[j];
+          cy = oy[j];
+          cz = oz[j];
+        }
+      const int wl = argmax_lane<A>(tv, ti);
+      __syncthreads();  // everyone is done reading the list before it is reused
+      if (lane == wl) {
+        rv_s[warp] = tv;
+        ri_s[warp] = ti;
+        rq_s[warp] = tj * NT + lane * NW + warp;
+        rx_s[warp][0] = cx;
+        rx_s[warp][1] = cy;
+        rx_s[warp][2] = cz;
+      }
+      __syncthreads();
+      if (warp == 0) {
+        const bits_t v = lane < NW ? rv_s[lane] : A::kmin;
+        const uint32_t i = lane < NW ? ri_s[lane] : kNoIdx;
+        const int gl = argmax_lane<A>(v, i);
+        if (lane == 0) {
+          sp_s[0][0] = rx_s[gl][0];
+          sp_s[0][1] = rx_s[gl][1];
+          sp_s[0][2] = rx_s[gl][2];
+          si_s[0] = ri_s[gl];
+          sq_s[0] = rq_s[gl];
+          order[k] = ri_s[gl];  // fps_core.py:167-168
+          sel[k] = A::from_bits(rv_s[gl]);
+          nsel_s = 1;
+        }
+      }
+    } else if (warp == 0) {
       bits_t lv[RPL];
       uint32_t li[RPL];
 #pragma unroll
       for (int t = 0; t < RPL; ++t) {
         const int e = lane + 32 * t;
-        lv[t] = e < NREC ? rv_s[e] : A::kmin;
-        li[t] = e < NREC ? ri_s[e] : kNoIdx;
+        lv[t] = e < ncand && e < NREC ? rv_s[e] : A::kmin;
+        li[t] = e < ncand && e < NREC ? ri_s[e] : kNoIdx;
       }
       unsigned taken = 0;
       int cand = -1;  // lane r holds the record of candidate r

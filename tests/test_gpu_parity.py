@@ -279,3 +279,20 @@ def test_bucketed_schedule_sizes_and_ties(cuda, dtype, sched):
             _check_batch(_cloud(rng, B, N, kind, dtype), min(m, N), rng.integers(0, N, size=B))
     finally:
         _device.set_schedule(prev)
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+def test_multi_winner_degenerate_ties(cuda, dtype):
+    """K1m when hundreds of bucket keys tie (identical points, exhausted
+    buckets): the candidate list overflows and rounds fall back to one exact
+    winner; results must still match the oracle."""
+    from paper_2604_17720_b200 import _device
+    prev = _device.set_schedule("multi")
+    try:
+        rng = np.random.default_rng(23)
+        for N, m in [(8000, 600), (20000, 3000)]:
+            pts = np.zeros((2, N, 3))
+            pts[:, : N // 50] = rng.random((2, N // 50, 3))  # 2% distinct, 98% duplicates
+            _check_batch(np.ascontiguousarray(pts.astype(dtype)), m, np.array([0, N - 1]))
+    finally:
+        _device.set_schedule(prev)
