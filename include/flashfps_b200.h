@@ -83,11 +83,13 @@ int ffps_run_kernel(int dtype, const void* xyz, int64_t batch,
  *   FFPS_ALGO_MULTI   K0 + K1m: the bucketed schedule taking up to 8 consecutive
  *                     greedy winners per reduction round (the longest prefix of
  *                     the top candidates provably unaffected by each other);
+ *   FFPS_ALGO_GRID    K0 + K1g: MULTI with the buckets indexed by a cell grid, so
+ *                     a selected point only tests the buckets within its reach;
  *   FFPS_ALGO_AUTO    BUCKET when n >= 2048 and (batch >= 48 or n >= 150000),
  *                     else STREAM (environment variable FFPS_ALGO=stream|bucket
  *                     overrides AUTO). */
 enum ffps_algo { FFPS_ALGO_AUTO = 0, FFPS_ALGO_STREAM = 1, FFPS_ALGO_BUCKET = 2,
-                 FFPS_ALGO_MULTI = 3 };
+                 FFPS_ALGO_MULTI = 3, FFPS_ALGO_GRID = 4 };
 
 /* Host -> device copy of the candidate prefix xyz[b][0:n_prefix) of every
  * cloud (the only coordinates a cache-on FlashFPS run reads,

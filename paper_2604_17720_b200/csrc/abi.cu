@@ -384,6 +384,121 @@ int run_bucketed(int dtype, const void* xyz, int64_t batch, int64_t cloud_stride
   return FFPS_OK;
 }
 
+// K1g: smallest bucket size whose bucket table + cell index fit shared memory
+int run_grid(int dtype, const void* xyz, int64_t batch, int64_t cloud_stride, int64_t n,
+             int64_t iters, const int64_t* seed_pos, const int64_t* index_map, int64_t map_stride,
+             int64_t* order, void* sel_d2, int64_t out_stride, cudaStream_t st, int dev) {
+  const DeviceInfo di = device_info(dev);
+  int cnt = 0;
+  const ffps::GridInst* insts = ffps::grid_instances(&cnt);
+  const ffps::GridInst* pick = nullptr;
+  int64_t nb = 0;
+  int G = 4;
+  size_t smem = 0;
+  for (int ppl = 1; ppl <= 8 && !pick; ppl *= 2) {
+    nb = (n + 32 * ppl - 1) / (32 * ppl);
+    if (nb > 65535) continue;
+    G = (int)std::lround(std::cbrt((double)nb / 2.0));
+    G = G < 4 ? 4 : (G > 16 ? 16 : G);
+    smem = ffps::grid_smem(dtype, nb, G);
+    if (smem + 12288 > di.smem_optin) continue;
+    for (int i = 0; i < cnt; ++i)
+      if (insts[i].dtype == dtype && insts[i].ppl == ppl) pick = &insts[i];
+  }
+  if (!pick) return fail(FFPS_EUNSUPPORTED, "no grid configuration for n=%lld", (long long)n);
+  const int64_t bs = 32 * pick->ppl;
+  const int64_t nslots = nb * bs;
+  const size_t esz = pick->esz;
+  const size_t per_cloud = (size_t)nslots * (7 * esz + 8) + (size_t)nb * 6 * esz;
+  unsigned char* scratch = nullptr;
+  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&scratch),
+                                  per_cloud * (size_t)batch + 256, st);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync(grid)");
+  const size_t arr = (size_t)nslots * esz * (size_t)batch;
+  ffps::BucketBuildParams bb;
+  bb.xyz = xyz;
+  bb.cloud_stride = cloud_stride;
+  bb.index_map = index_map;
+  bb.map_stride = map_stride;
+  bb.n = n;
+  bb.X = scratch;
+  bb.Y = scratch + arr;
+  bb.Z = scratch + 2 * arr;
+  bb.D = scratch + 3 * arr;
+  bb.BB = scratch + 4 * arr;
+  bb.O = reinterpret_cast<int32_t*>(scratch + 4 * arr + (size_t)nb * 6 * esz * (size_t)batch);
+  bb.nslots = nslots;
+  bb.nbuckets = nb;
+  bb.bs = bs;
+  {
+    unsigned char* t = reinterpret_cast<unsigned char*>(bb.O) + (size_t)nslots * 4 * (size_t)batch;
+    bb.TX = t;
+    bb.TY = t + arr;
+    bb.TZ = t + 2 * arr;
+    bb.TO = reinterpret_cast<int32_t*>(t + 3 * arr);
+  }
+  e = ffps::launch_bucket_build(dtype, bb, batch, st);
+  if (e != cudaSuccess) {
+    cudaFreeAsync(scratch, st);
+    return cuda_fail(e, "bucket_build_kernel launch");
+  }
+  ffps::BucketParams prm;
+  prm.X = bb.X;
+  prm.Y = bb.Y;
+  prm.Z = bb.Z;
+  prm.D = bb.D;
+  prm.O = bb.O;
+  prm.BB = bb.BB;
+  prm.nslots = nslots;
+  prm.nbuckets = nb;
+  prm.xyz = xyz;
+  prm.cloud_stride = cloud_stride;
+  prm.index_map = index_map;
+  prm.map_stride = map_stride;
+  prm.iters = iters;
+  prm.seed_pos = seed_pos;
+  prm.order = order;
+  prm.sel_d2 = sel_d2;
+  prm.out_stride = out_stride;
+  prm.neg_zero = -0.0f;
+  prm.trace = nullptr;
+  prm.trace_iters = 0;
+  if (const char* tr = getenv("FFPS_TRACE_GRID")) {
+    unsigned long long ptr = 0;
+    long long it = 0;
+    if (sscanf(tr, "%llu,%lld", &ptr, &it) == 2) {
+      prm.trace = reinterpret_cast<long long*>(ptr);
+      prm.trace_iters = it;
+    }
+  }
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    auto key = std::make_pair(dev, pick->fn);
+    if (!g_attr_done.count(key)) {
+      cudaFuncAttributes fa;
+      e = cudaFuncGetAttributes(&fa, pick->fn);
+      if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(pick->fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)(device_info_nolock(dev).smem_optin - fa.sharedSizeBytes));
+      if (e != cudaSuccess) {
+        cudaFreeAsync(scratch, st);
+        return cuda_fail(e, "cudaFuncSetAttribute(grid)");
+      }
+      g_attr_done[key] = true;
+    }
+  }
+  void* args[] = {&prm, &G};
+  e = cudaLaunchKernel(pick->fn, dim3((unsigned)batch), dim3(pick->nt), args, smem, st);
+  if (e != cudaSuccess) {
+    cudaFreeAsync(scratch, st);
+    return cuda_fail(e, "fps_grid_kernel launch");
+  }
+  g_last_launches = 2;
+  e = cudaFreeAsync(scratch, st);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaFreeAsync(grid)");
+  return FFPS_OK;
+}
+
 int run_streaming(int dtype, const void* xyz, int64_t batch, int64_t cloud_stride, int64_t n,
                   int64_t iters, const int64_t* seed_pos, const int64_t* index_map,
                   int64_t map_stride, int64_t* order, void* sel_d2, int64_t out_stride,
@@ -473,6 +588,7 @@ int resolve_algo(int algo, int64_t n, int64_t batch) {
     if (env && strcmp(env, "stream") == 0) return FFPS_ALGO_STREAM;
     if (env && strcmp(env, "bucket") == 0) return FFPS_ALGO_BUCKET;
     if (env && strcmp(env, "multi") == 0) return FFPS_ALGO_MULTI;
+    if (env && strcmp(env, "grid") == 0) return FFPS_ALGO_GRID;
     return n >= kAutoBucketMin && (batch >= kAutoBucketBatch || n >= kAutoBucketLarge)
                ? FFPS_ALGO_BUCKET
                : FFPS_ALGO_STREAM;
@@ -529,7 +645,7 @@ int ffps_run_kernel_ex(int dtype, const void* xyz, int64_t batch, int64_t cloud_
   if (dtype != FFPS_F32 && dtype != FFPS_F64)
     return fail(FFPS_EINVAL, "dtype must be FFPS_F32 or FFPS_F64");
   if (algo != FFPS_ALGO_AUTO && algo != FFPS_ALGO_STREAM && algo != FFPS_ALGO_BUCKET &&
-      algo != FFPS_ALGO_MULTI)
+      algo != FFPS_ALGO_MULTI && algo != FFPS_ALGO_GRID)
     return fail(FFPS_EINVAL, "unknown algorithm %d", algo);
   if (batch < 0) return fail(FFPS_EINVAL, "batch=%lld < 0", (long long)batch);
   if (batch == 0) return FFPS_OK;
@@ -546,6 +662,9 @@ int ffps_run_kernel_ex(int dtype, const void* xyz, int64_t batch, int64_t cloud_
   if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int a = resolve_algo(algo, n, batch);
+  if (a == FFPS_ALGO_GRID)
+    return run_grid(dtype, xyz, batch, cloud_stride, n, iters, seed_pos, index_map, map_stride,
+                    order, sel_d2, out_stride, st, dev);
   if (a == FFPS_ALGO_BUCKET || a == FFPS_ALGO_MULTI)
     return run_bucketed(dtype, xyz, batch, cloud_stride, n, iters, seed_pos, index_map,
                         map_stride, order, sel_d2, out_stride, st, dev, a == FFPS_ALGO_MULTI);

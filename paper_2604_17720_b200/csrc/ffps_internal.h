@@ -100,6 +100,17 @@ struct BucketInst {
 
 const BucketInst* bucket_instances(int* count);
 const BucketInst* multi_instances(int* count);  // K1m (fps_multi.cu)
+
+// K1g (fps_grid.cu): multi-winner rounds with a cell index of the buckets
+struct GridInst {
+  int dtype;
+  int nt;
+  int ppl;
+  const void* fn;  // fps_grid_kernel(BucketParams, int G)
+  size_t esz;
+};
+const GridInst* grid_instances(int* count);
+size_t grid_smem(int dtype, int64_t nb, int G);
 size_t bucket_build_smem();
 cudaError_t launch_bucket_build(int dtype, const BucketBuildParams& p, int64_t batch,
                                 cudaStream_t st);

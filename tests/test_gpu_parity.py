@@ -16,7 +16,7 @@ from oracle import oracle
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(params=["stream", "bucket", "multi"])
+@pytest.fixture(params=["stream", "bucket", "multi", "grid"])
 def schedule(request):
     """Run the test under each greedy schedule (K1 streaming, K0+K1b bucketed)."""
     from paper_2604_17720_b200 import _device
@@ -261,7 +261,7 @@ def test_abi_rejects_bad_arguments(cuda):
     assert lib.ffps_fill_slice(0, 1, 1, 1, 10, 5, 4, None) == -1
 
 
-@pytest.mark.parametrize("sched", ["bucket", "multi"])
+@pytest.mark.parametrize("sched", ["bucket", "multi", "grid"])
 @pytest.mark.parametrize("dtype", [np.float32, np.float64])
 def test_bucketed_schedule_sizes_and_ties(cuda, dtype, sched):
     """K0+K1b / K0+K1m forced on every size class: n below / at / above one
@@ -282,12 +282,13 @@ def test_bucketed_schedule_sizes_and_ties(cuda, dtype, sched):
 
 
 @pytest.mark.parametrize("dtype", [np.float32, np.float64])
-def test_multi_winner_degenerate_ties(cuda, dtype):
+@pytest.mark.parametrize("sched", ["multi", "grid"])
+def test_multi_winner_degenerate_ties(cuda, dtype, sched):
     """K1m when hundreds of bucket keys tie (identical points, exhausted
     buckets): the candidate list overflows and rounds fall back to one exact
     winner; results must still match the oracle."""
     from paper_2604_17720_b200 import _device
-    prev = _device.set_schedule("multi")
+    prev = _device.set_schedule(sched)
     try:
         rng = np.random.default_rng(23)
         for N, m in [(8000, 600), (20000, 3000)]:

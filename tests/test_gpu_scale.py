@@ -22,7 +22,7 @@ from oracle import oracle
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(params=["stream", "bucket", "multi"])
+@pytest.fixture(params=["stream", "bucket", "multi", "grid"])
 def schedule(request):
     prev = _device.set_schedule(request.param)
     yield request.param

@@ -19,12 +19,14 @@ def main():
     ap.add_argument("--n", type=int, default=50000)
     ap.add_argument("--iters", type=int, default=12500)
     ap.add_argument("--nw", type=int, default=16)
+    ap.add_argument("--sched", default="multi", choices=["multi", "grid"])
     a = ap.parse_args()
     g = torch.Generator(device="cuda").manual_seed(0)
     x = torch.rand((a.batch, a.n, 3), generator=g, device="cuda", dtype=torch.float64).float()
     tr = torch.zeros((a.nw, a.iters, 8), dtype=torch.int64, device="cuda")
-    os.environ["FFPS_TRACE_MULTI"] = f"{tr.data_ptr()},{a.iters}"
-    prev = _device.set_schedule("multi")
+    os.environ["FFPS_TRACE_MULTI" if a.sched == "multi" else "FFPS_TRACE_GRID"] = \
+        f"{tr.data_ptr()},{a.iters}"
+    prev = _device.set_schedule(a.sched)
     B = a.batch
     order = torch.empty((B, a.iters), dtype=torch.int64, device="cuda")
     sel = torch.empty((B, a.iters), dtype=x.dtype, device="cuda")
@@ -38,13 +40,16 @@ def main():
     nsel = t[0, :, 5]
     print(f"rounds {R} for {a.iters} iterations: {nsel.sum() + 1} winners, "
           f"{(nsel.sum()) / R:.2f} per round")
-    names = ["bound", "reeval", "topk", "merge+barriers"]
+    names = (["bound", "reeval", "topk", "merge+barriers"] if a.sched == "multi" else
+             ["flag", "reeval", "candidates", "merge+barriers"])
     ph = np.stack([t[:, :, i + 1] - t[:, :, i] for i in range(4)], -1)
     for lo, hi in [(1, max(2, R // 10)), (R // 10, R)]:
         sl = slice(lo, hi)
         tot = t[0, sl, 4] - t[0, sl, 0]
+        flagged = t[0, sl, 6] if a.sched == "grid" else t[:, sl, 6].sum(0)
         print(f"rounds [{lo},{hi}): cycles/round median {np.median(tot):.0f}, winners/round "
-              f"{nsel[sl].mean():.2f}, flagged/round {t[:, sl, 6].sum(0).mean():.1f}")
+              f"{nsel[sl].mean():.2f}, flagged/round {flagged.mean():.1f}" +
+              (f", full-scan rounds {t[0, sl, 7].mean():.2f}" if a.sched == "grid" else ""))
         for i, nm in enumerate(names):
             v = ph[:, sl, i]
             print(f"   {nm:15s} mean {v.mean():7.0f}  max-warp mean {v.max(0).mean():7.0f}")
