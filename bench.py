@@ -398,7 +398,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         ex_step, ex_kern = arm(cfg_exh, False, "auto", ks)
         exh = {"value": global_batch / (ex_step / 1e3), "unit": "clouds/s",
                "ms_per_step": ex_step, "ms_per_cloud": ex_step / B, "steps": ks,
-               "schedule": "auto (bucketed K0+K1b)",
+               "schedule": "auto (" + _native.auto_schedule(args.n, B) + ")",
                "stage1_kernel_ms": float(np.mean([k[3] for k in ex_kern if k[1] == args.n])),
                "units_per_step": ex_units,
                "speedup_flash_vs_exhaustive": ex_step / ms_step}
@@ -439,8 +439,9 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     kms = float(np.mean([k[3] for k in kern])) if kern else float("nan")
     pk = peaks()
     achieved = units_launch * BYTES_PER_UNIT_F32 / (kms / 1e3) / 1e9
-    plan = {"schedule": "bucket", **_native.bucket_plan(_native.F32, c1)} \
-        if c1 >= 2048 and (B >= 48 or c1 >= 150000) else \
+    sched = _native.auto_schedule(c1, B)
+    plan = {"schedule": sched, **_native.bucket_plan(_native.F32, c1)} \
+        if sched in ("bucket", "multi", "grid") else \
         {"schedule": "stream", **_native.plan(_native.F32, c1, B)}
     sm_mhz = clocks["sm_mhz"] or pk["sm_max_mhz"]
     issue_ceiling = 148 * 128 * sm_mhz * 1e6 / 9.0   # ~9 FP32-pipe instr / unit
@@ -448,15 +449,18 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     try:  # per-launch DRAM bytes of the same kernel from one `ncu --set full` capture
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
             tj = json.load(fh)
-        kname = "fps_bucket_kernel" if plan["schedule"] == "bucket" else "fps_greedy_kernel"
+        kname = {"bucket": "fps_bucket_kernel", "multi": "fps_multi_kernel",
+                 "grid": "fps_grid_kernel"}.get(plan["schedule"], "fps_greedy_kernel")
         hit = [v for k_, v in tj.items() if kname in k_]
         traffic = hit[0]["dram_bytes"] if hit else None
     except (OSError, ValueError, KeyError):
         traffic = None
     roof = {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
             "frac": achieved / pk["hbm_gbs"], "traffic": traffic,
-            "kernel": "fps_bucket_kernel (K1b)" if plan["schedule"] == "bucket"
-                      else "fps_greedy_kernel (K1)", "kernel_ms": kms,
+            "kernel": {"bucket": "fps_bucket_kernel (K1b)", "multi": "fps_multi_kernel (K1m)",
+                       "grid": "fps_grid_kernel (K1g)"}.get(plan["schedule"],
+                                                           "fps_greedy_kernel (K1)"),
+            "kernel_ms": kms,
             "units_per_launch": units_launch, "bytes_per_unit": BYTES_PER_UNIT_F32,
             "peak_src": pk["src"],
             "note": ("algorithmic bytes of the standard streaming FPS (20 B per point-"

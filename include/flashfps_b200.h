@@ -85,9 +85,9 @@ int ffps_run_kernel(int dtype, const void* xyz, int64_t batch,
  *                     the top candidates provably unaffected by each other);
  *   FFPS_ALGO_GRID    K0 + K1g: MULTI with the buckets indexed by a cell grid, so
  *                     a selected point only tests the buckets within its reach;
- *   FFPS_ALGO_AUTO    BUCKET when n >= 2048 and (batch >= 48 or n >= 150000),
- *                     else STREAM (environment variable FFPS_ALGO=stream|bucket
- *                     overrides AUTO). */
+ *   FFPS_ALGO_AUTO    GRID for n >= 65536; BUCKET for n >= 2048 and batch >= 48;
+ *                     else STREAM (the environment variable
+ *                     FFPS_ALGO=stream|bucket|multi|grid overrides AUTO). */
 enum ffps_algo { FFPS_ALGO_AUTO = 0, FFPS_ALGO_STREAM = 1, FFPS_ALGO_BUCKET = 2,
                  FFPS_ALGO_MULTI = 3, FFPS_ALGO_GRID = 4 };
 

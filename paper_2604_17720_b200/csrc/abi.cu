@@ -570,15 +570,15 @@ int run_streaming(int dtype, const void* xyz, int64_t batch, int64_t cloud_strid
   return FFPS_OK;
 }
 
-// FFPS_ALGO_AUTO (measured on B200, tools/bench_configs.py): the bucketed
-// schedule runs one CTA per cloud and wins when the batch alone fills the GPU
-// (>= 48 clouds) or the clouds are so large that the streaming schedule runs
-// in several waves / spills (>= 150K points); below that the streaming
-// schedule spreads each cloud over many SMs and wins.  FFPS_ALGO in the
-// environment ("stream" / "bucket") overrides AUTO for sweeps.
+// FFPS_ALGO_AUTO (measured on B200, tools/sweep_schedules.sh,
+// profiles/r01_schedules.jsonl): GRID (multi-winner rounds + cell index) for
+// clouds of >= 64K points at any batch; BUCKET when the batch alone fills the
+// GPU (>= 48 clouds of >= 2048 points); STREAM otherwise (few small clouds:
+// the cluster kernel spreads each cloud over many SMs).  FFPS_ALGO in the
+// environment ("stream" / "bucket" / "multi" / "grid") overrides AUTO.
 constexpr int64_t kAutoBucketMin = 2048;
 constexpr int64_t kAutoBucketBatch = 48;
-constexpr int64_t kAutoBucketLarge = 150000;
+constexpr int64_t kAutoGridMin = 65536;
 
 int resolve_algo(int algo, int64_t n, int64_t batch) {
   if (algo == FFPS_ALGO_AUTO) {
@@ -589,9 +589,9 @@ int resolve_algo(int algo, int64_t n, int64_t batch) {
     if (env && strcmp(env, "bucket") == 0) return FFPS_ALGO_BUCKET;
     if (env && strcmp(env, "multi") == 0) return FFPS_ALGO_MULTI;
     if (env && strcmp(env, "grid") == 0) return FFPS_ALGO_GRID;
-    return n >= kAutoBucketMin && (batch >= kAutoBucketBatch || n >= kAutoBucketLarge)
-               ? FFPS_ALGO_BUCKET
-               : FFPS_ALGO_STREAM;
+    if (n >= kAutoGridMin) return FFPS_ALGO_GRID;
+    return n >= kAutoBucketMin && batch >= kAutoBucketBatch ? FFPS_ALGO_BUCKET
+                                                            : FFPS_ALGO_STREAM;
   }
   return algo;
 }

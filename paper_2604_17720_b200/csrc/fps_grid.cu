@@ -27,8 +27,9 @@
 //      position, xyz) and second-best value into the bucket table
 //   | barrier |
 //   C. per-warp max over a contiguous slice of the table | barrier | every key
-//      >= the smallest warp max joins the candidate list | barrier |
-//   D. warp 0: top-KM candidates, chain test (K1m), accepted prefix | barrier |
+//      >= tau, the KM-th largest warp max, joins the candidate list | barrier |
+//   D. every warp: top-KM of the list by rank, chain test (K1m), accepted
+//      prefix into its own copy (identical in all warps, no barrier)
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -85,7 +86,7 @@ __global__ void __launch_bounds__(NT, 1) fps_grid_kernel(const BucketParams prm,
   constexpr int NREC = 128;
   constexpr int RPL = NREC / 32;
   static_assert(KM <= 32, "one candidate per lane in the chain test");
-  static_assert(NW >= 2, "two warps per selected point");
+  static_assert(NW >= 2 && NW >= KM, "two warps per point, KM warp maxima");
 
   const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nb = (int)prm.nbuckets;
@@ -115,11 +116,13 @@ __global__ void __launch_bounds__(NT, 1) fps_grid_kernel(const BucketParams prm,
   __shared__ uint32_t ri_s[NREC];
   __shared__ int32_t rq_s[NREC];
   __shared__ T rx_s[NREC][3];
-  __shared__ T sp_s[KM][3];
-  __shared__ uint32_t si_s[KM];
-  __shared__ int32_t sq_s[KM];
-  __shared__ int nsel_s, ncand_s, rcount_s, ocount_s;
-  __shared__ bits_t rmax_s;  // upper bound of every key (R^2 of the cube)
+  // accepted points of the last round: every warp keeps its own copy (all
+  // warps derive the same set from the candidate list, no barrier needed)
+  __shared__ T sp_w[NW][KM][3];
+  __shared__ uint32_t si_w[NW][KM];
+  __shared__ int32_t sq_w[NW][KM];
+  __shared__ int16_t top_w[NW][KM];
+  __shared__ int ncand_s, rcount_s, ocount_s;
   __shared__ T glo_s[3], ginv_s[3];
   __shared__ T red_s[2][NW][3];
   __shared__ uint32_t cscr_s[NW][2][32];  // per-warp cell scratch of the flag phase
@@ -220,19 +223,21 @@ __global__ void __launch_bounds__(NT, 1) fps_grid_kernel(const BucketParams prm,
   const int seed = (int)prm.seed_pos[b];
   int64_t* order = prm.order + (int64_t)b * prm.out_stride;
   T* sel = static_cast<T*>(prm.sel_d2) + (int64_t)b * prm.out_stride;
-  if (tid == 0) {
+  if (lane == 0) {
     const T* X0 = static_cast<const T*>(prm.xyz) + (int64_t)b * prm.cloud_stride * 3;
     const int64_t src = prm.index_map ? prm.index_map[(int64_t)b * prm.map_stride + seed] : seed;
-    sp_s[0][0] = X0[3 * src + 0];
-    sp_s[0][1] = X0[3 * src + 1];
-    sp_s[0][2] = X0[3 * src + 2];
-    si_s[0] = (uint32_t)seed;
-    sq_s[0] = -1;
-    nsel_s = 1;
-    rmax_s = A::bits(A::pinf());
+    sp_w[warp][0][0] = X0[3 * src + 0];
+    sp_w[warp][0][1] = X0[3 * src + 1];
+    sp_w[warp][0][2] = X0[3 * src + 2];
+    si_w[warp][0] = (uint32_t)seed;
+    sq_w[warp][0] = -1;
+  }
+  if (tid == 0) {
     order[0] = seed;
     sel[0] = A::pinf();
   }
+  int J = 1;                        // points accepted by the last round
+  bits_t rmax = A::bits(A::pinf());  // upper bound of every key (R^2 of the cube)
   __syncthreads();
   const int iters = (int)prm.iters;
   const int nover = ocount_s;
@@ -246,14 +251,27 @@ __global__ void __launch_bounds__(NT, 1) fps_grid_kernel(const BucketParams prm,
   auto test = [&](int q, int t, T px, T py, T pz) {  // K1b's exact bound test
     if (!(box_lb(px, py, pz, box + (size_t)q * 6) >= A::from_bits(kv[q]))) flag(q, t);
   };
+  // warp-converged variant: every lane calls it (valid = has a bucket to test);
+  // new buckets are appended with one shared-memory atomic per warp
+  auto test_warp = [&](bool valid, int q, int t, T px, T py, T pz) {
+    bool isnew = false;
+    if (valid && !(box_lb(px, py, pz, box + (size_t)q * 6) >= A::from_bits(kv[q])))
+      isnew = atomicOr(&pmask[q], 1u << t) == 0u;
+    const unsigned m = __ballot_sync(0xffffffffu, isnew);
+    if (m) {
+      int base = 0;
+      if (lane == __ffs(m) - 1) base = atomicAdd(&rcount_s, __popc(m));
+      base = __shfl_sync(0xffffffffu, base, __ffs(m) - 1);
+      if (isnew) rlist[base + __popc(m & ((1u << lane) - 1u))] = q;
+    }
+  };
 
   int k = 1;
   for (int round = 0; k < iters; ++round) {
-    const int J = nsel_s;
     long long t0 = 0, t1 = 0, t2 = 0, t3 = 0;
     if (trace) t0 = clock64();
     // A. flag ---------------------------------------------------------------------
-    const T r2 = A::from_bits(rmax_s);
+    const T r2 = A::from_bits(rmax);
     // half-width of the search cube, padded for the rounding of p +- R
     const T R = round == 0 ? A::pinf() : (T)(sqrt((double)r2) * 1.001) ;
     bool full = round == 0 || !(R * ginv[0] < T(3)) || !(R * ginv[1] < T(3)) ||
@@ -264,9 +282,10 @@ __global__ void __launch_bounds__(NT, 1) fps_grid_kernel(const BucketParams prm,
           flag(q, 0);
           continue;
         }
-        for (int t = 0; t < J; ++t) test(q, t, sp_s[t][0], sp_s[t][1], sp_s[t][2]);
+        for (int t = 0; t < J; ++t) test(q, t, sp_w[warp][t][0], sp_w[warp][t][1], sp_w[warp][t][2]);
       }
-      if (round > 0 && tid < J && sq_s[tid] >= 0) flag(sq_s[tid], tid);  // the point -> -inf
+      if (round > 0 && warp == 0 && lane < J && sq_w[0][lane] >= 0)
+        flag(sq_w[0][lane], lane);  // the point -> -inf
     } else {
       // two warps per point (NW >= 2 * KM); the (cell, entry) pairs of the
       // point's cube are spread over the 64 lanes: per chunk of 32 cells the
@@ -274,7 +293,7 @@ __global__ void __launch_bounds__(NT, 1) fps_grid_kernel(const BucketParams prm,
       // shared scratch, then every lane walks flat entry indices
       for (int t = warp >> 1; t < J; t += NW / 2) {
         const int half = warp & 1;
-        const T px = sp_s[t][0], py = sp_s[t][1], pz = sp_s[t][2];
+        const T px = sp_w[warp][t][0], py = sp_w[warp][t][1], pz = sp_w[warp][t][2];
         const T pad = (fabs(px) + fabs(py) + fabs(pz) + T(1)) * T(1e-6);
         int c0[3], c1[3];
         const T pc[3] = {px, py, pz};
@@ -306,20 +325,28 @@ __global__ void __launch_bounds__(NT, 1) fps_grid_kernel(const BucketParams prm,
           cs[lane] = e0;
           ci[lane] = incl;
           __syncwarp();
-          for (uint32_t f = lane + 32 * half; f < total; f += 64) {
-            int lo_l = 0, hi_l = 31;  // lowest cell whose inclusive count > f
-            while (lo_l < hi_l) {
-              const int mid = (lo_l + hi_l) >> 1;
-              if (ci[mid] > f) hi_l = mid;
-              else lo_l = mid + 1;
+          for (uint32_t f0 = 32 * half; f0 < total; f0 += 64) {  // uniform trip count
+            const uint32_t f = f0 + lane;
+            int q = 0;
+            if (f < total) {
+              int lo_l = 0, hi_l = 31;  // lowest cell whose inclusive count > f
+              while (lo_l < hi_l) {
+                const int mid = (lo_l + hi_l) >> 1;
+                if (ci[mid] > f) hi_l = mid;
+                else lo_l = mid + 1;
+              }
+              const uint32_t before = lo_l == 0 ? 0u : ci[lo_l - 1];
+              q = cent[cs[lo_l] + (f - before)];
             }
-            const uint32_t before = lo_l == 0 ? 0u : ci[lo_l - 1];
-            test(cent[cs[lo_l] + (f - before)], t, px, py, pz);
+            test_warp(f < total, q, t, px, py, pz);
           }
           __syncwarp();
         }
-        for (int i = lane + 32 * half; i < nover; i += 64) test(olist[i], t, px, py, pz);
-        if (lane == 0 && half == 0 && sq_s[t] >= 0) flag(sq_s[t], t);  // the point -> -inf
+        for (int i0 = 32 * half; i0 < nover; i0 += 64) {
+          const int i = i0 + lane;
+          test_warp(i < nover, i < nover ? olist[i] : 0, t, px, py, pz);
+        }
+        if (lane == 0 && half == 0 && sq_w[warp][t] >= 0) flag(sq_w[warp][t], t);  // -> -inf
       }
     }
     if (trace) t1 = clock64();
@@ -353,8 +380,8 @@ __global__ void __launch_bounds__(NT, 1) fps_grid_kernel(const BucketParams prm,
         while (m) {  // only the points that flagged the bucket can change it
           const int t = __ffs(m) - 1;
           m &= m - 1u;
-          const T px = sp_s[t][0], py = sp_s[t][1], pz = sp_s[t][2];
-          const uint32_t pw = si_s[t];
+          const T px = sp_w[warp][t][0], py = sp_w[warp][t][1], pz = sp_w[warp][t][2];
+          const uint32_t pw = si_w[warp][t];
 #pragma unroll
           for (int u = 0; u < PPL; ++u) {
             T nd = A::vmin(ds[c][u], A::d2(xs[c][u], ys[c][u], zs[c][u], px, py, pz));  // :93
@@ -418,9 +445,20 @@ __global__ void __launch_bounds__(NT, 1) fps_grid_kernel(const BucketParams prm,
     }
     __syncthreads();
     {
-      bits_t tau = A::bits(A::pinf());
+      // tau = the KM-th largest warp maximum: KM warps hold a key >= tau, so
+      // the global top-KM is among the keys >= tau (ties at tau included)
+      bits_t tau;
+      {
+        const bits_t mine = lane < NW ? wm_s[lane] : A::kmin;
+        int rank = 0;
 #pragma unroll
-      for (int w = 0; w < NW; ++w) tau = wm_s[w] < tau ? wm_s[w] : tau;
+        for (int w = 0; w < NW; ++w) {
+          const bits_t o = wm_s[w];
+          rank += (o > mine || (o == mine && w < lane)) ? 1 : 0;
+        }
+        const unsigned hit = __ballot_sync(0xffffffffu, lane < NW && rank == KM - 1);
+        tau = A::shfl(mine, hit ? __ffs(hit) - 1 : 0);
+      }
       for (int q0 = s0; q0 < s1; q0 += 32) {
         const int q = q0 + lane;
         const bool c = q < s1 && kv[q] >= tau && kv[q] != A::kmin;
@@ -444,103 +482,90 @@ __global__ void __launch_bounds__(NT, 1) fps_grid_kernel(const BucketParams prm,
     }
     if (trace) t3 = clock64();
     __syncthreads();  // candidate list complete
-    // D. warp 0: top-KM, chain test, accepted prefix ---------------------------------
+    // D. every warp: top-KM of the list by rank, chain test, accepted prefix --------
+    //    (identical in all warps; warp 0 reports them)
     const int ncand = ncand_s;
-    if (warp == 0) {
-      int acc = 1;
-      int cand = -1;
-      T cx = T(0), cy = T(0), cz = T(0);
-      bits_t cv = A::kmin;
-      if (ncand > NREC) {
-        // massive ties: one exact winner from the whole table this round
-        bits_t bv = A::kmin;
-        uint32_t bi = kNoIdx;
-        int bq = 0;
-        for (int q = lane; q < nb; q += 32)
-          if (kv[q] > bv || (kv[q] == bv && ki[q] < bi)) {
-            bv = kv[q];
-            bi = ki[q];
-            bq = q;
-          }
-        const int wl = argmax_lane_g<A>(bv, bi);
-        const int q = __shfl_sync(0xffffffffu, bq, wl);
-        if (lane == 0) {
-          sp_s[0][0] = kx[q * 3 + 0];
-          sp_s[0][1] = kx[q * 3 + 1];
-          sp_s[0][2] = kx[q * 3 + 2];
-          si_s[0] = ki[q];
-          sq_s[0] = q;
+    int acc = 1;
+    if (ncand > NREC) {
+      // massive ties: one exact winner from the whole table this round
+      bits_t bv = A::kmin;
+      uint32_t bi = kNoIdx;
+      int bq = 0;
+      for (int q = lane; q < nb; q += 32)
+        if (kv[q] > bv || (kv[q] == bv && ki[q] < bi)) {
+          bv = kv[q];
+          bi = ki[q];
+          bq = q;
+        }
+      const int wl = argmax_lane_g<A>(bv, bi);
+      const int q = __shfl_sync(0xffffffffu, bq, wl);
+      if (lane == 0) {
+        sp_w[warp][0][0] = kx[q * 3 + 0];
+        sp_w[warp][0][1] = kx[q * 3 + 1];
+        sp_w[warp][0][2] = kx[q * 3 + 2];
+        si_w[warp][0] = ki[q];
+        sq_w[warp][0] = q;
+        if (warp == 0) {
           order[k] = ki[q];  // fps_core.py:167-168
           sel[k] = A::from_bits(kv[q]);
-          rmax_s = kv[q];
         }
-      } else {
-        bits_t lv[RPL];
-        uint32_t li[RPL];
-#pragma unroll
-        for (int t = 0; t < RPL; ++t) {
-          const int e = lane + 32 * t;
-          lv[t] = e < ncand ? rv_s[e] : A::kmin;
-          li[t] = e < ncand ? ri_s[e] : kNoIdx;
+      }
+      rmax = kv[q];
+    } else {
+      // rank of every list entry = number of larger keys (value desc, position asc)
+      for (int e = lane; e < ncand; e += 32) {
+        const bits_t v = rv_s[e];
+        const uint32_t i = ri_s[e];
+        int rank = 0;
+        for (int e2 = 0; e2 < ncand && rank < KM; ++e2) {
+          const bits_t v2 = rv_s[e2];
+          rank += (v2 > v || (v2 == v && ri_s[e2] < i)) ? 1 : 0;
         }
-        unsigned taken = 0;
-#pragma unroll 1
-        for (int r = 0; r < KM; ++r) {
-          bits_t bv = A::kmin;
-          uint32_t bi = kNoIdx;
-          int bt = 0;
-#pragma unroll
-          for (int t = 0; t < RPL; ++t)
-            if (!((taken >> t) & 1u) && (lv[t] > bv || (lv[t] == bv && li[t] < bi))) {
-              bv = lv[t];
-              bi = li[t];
-              bt = t;
-            }
-          const int wl = argmax_lane_g<A>(bv, bi);
-          if (lane == wl) taken |= 1u << bt;
-          const int e = __shfl_sync(0xffffffffu, lane + 32 * bt, wl);
-          if (lane == r) cand = e;
-        }
-        const bool live = lane < KM && cand >= 0 && cand < ncand;
-        cv = live ? rv_s[cand] : A::kmin;
-        const bits_t c2 = live ? r2_s[cand] : A::kmin;
-        cx = live ? rx_s[cand][0] : T(0);
-        cy = live ? rx_s[cand][1] : T(0);
-        cz = live ? rx_s[cand][2] : T(0);
-        bool ok = live && A::from_bits(cv) >= T(0);
-        for (int bb = 0; bb < KM - 1; ++bb) {
-          const T bx = __shfl_sync(0xffffffffu, cx, bb);
-          const T by = __shfl_sync(0xffffffffu, cy, bb);
-          const T bz = __shfl_sync(0xffffffffu, cz, bb);
-          const bits_t b2 = A::shfl(c2, bb);
-          if (bb < lane && ok)
-            ok = !(A::d2(cx, cy, cz, bx, by, bz) < A::from_bits(cv)) && cv > b2;  // (a), (b)
-        }
-        const unsigned okm = __ballot_sync(0xffffffffu, ok || lane == 0);
-        acc = __ffs(~okm) - 1;
-        if (acc < 0 || acc > KM) acc = KM;
-        if (acc > iters - k) acc = iters - k;
-        if (lane < acc) {
-          sp_s[lane][0] = cx;
-          sp_s[lane][1] = cy;
-          sp_s[lane][2] = cz;
-          si_s[lane] = ri_s[cand];
-          sq_s[lane] = rq_s[cand];
+        if (rank < KM) top_w[warp][rank] = (int16_t)e;
+      }
+      __syncwarp();
+      const int nc = ncand < KM ? ncand : KM;
+      const bool live = lane < nc;
+      const int cand = live ? top_w[warp][lane] : 0;
+      const bits_t cv = live ? rv_s[cand] : A::kmin;
+      const bits_t c2 = live ? r2_s[cand] : A::kmin;
+      const T cx = live ? rx_s[cand][0] : T(0);
+      const T cy = live ? rx_s[cand][1] : T(0);
+      const T cz = live ? rx_s[cand][2] : T(0);
+      bool ok = live && A::from_bits(cv) >= T(0);
+      for (int bb = 0; bb < KM - 1; ++bb) {
+        const T bx = __shfl_sync(0xffffffffu, cx, bb);
+        const T by = __shfl_sync(0xffffffffu, cy, bb);
+        const T bz = __shfl_sync(0xffffffffu, cz, bb);
+        const bits_t b2 = A::shfl(c2, bb);
+        if (bb < lane && ok)
+          ok = !(A::d2(cx, cy, cz, bx, by, bz) < A::from_bits(cv)) && cv > b2;  // (a), (b)
+      }
+      const unsigned okm = __ballot_sync(0xffffffffu, ok || lane == 0);
+      acc = __ffs(~okm) - 1;
+      if (acc < 0 || acc > KM) acc = KM;
+      if (acc > iters - k) acc = iters - k;
+      if (lane < acc) {
+        sp_w[warp][lane][0] = cx;
+        sp_w[warp][lane][1] = cy;
+        sp_w[warp][lane][2] = cz;
+        si_w[warp][lane] = ri_s[cand];
+        sq_w[warp][lane] = rq_s[cand];
+        if (warp == 0) {
           order[k + lane] = ri_s[cand];  // fps_core.py:167-168
           sel[k + lane] = A::from_bits(cv);
         }
-        const bits_t first = A::shfl(cv, 0);
-        if (lane == 0) rmax_s = first;
       }
-      if (lane == 0) nsel_s = acc;
+      rmax = A::shfl(cv, 0);
     }
-    __syncthreads();  // accepted points visible
+    __syncwarp();
+    J = acc;
     if (trace && round < prm.trace_iters) {
       long long* rr = trace + (int64_t)round * 8;
-      rr[0] = t0; rr[1] = t1; rr[2] = t2; rr[3] = t3; rr[4] = clock64(); rr[5] = nsel_s;
+      rr[0] = t0; rr[1] = t1; rr[2] = t2; rr[3] = t3; rr[4] = clock64(); rr[5] = acc;
       rr[6] = nr; rr[7] = full;
     }
-    k += nsel_s;
+    k += acc;
   }
 
   // positions -> original indices for restricted runs (fps_cache.py:197)
