@@ -42,7 +42,8 @@ namespace ffps {
 
 namespace {
 
-constexpr int kMaxCells = 8;  // a bucket registered in at most this many cells
+constexpr int kMaxCells = 27;  // a bucket registered in at most this many cells
+constexpr int kEntryBudget = 12;  // cell entries per bucket on average (shared budget)
 
 template <typename A>
 __device__ __forceinline__ int argmax_lane_g(typename A::bits_t v, uint32_t i) {
@@ -72,7 +73,7 @@ template <typename T>
 __host__ __device__ constexpr size_t grid_smem_bytes(int64_t nb, int G) {
   return (size_t)nb * (6 * sizeof(T) + 3 * sizeof(T) + 2 * sizeof(typename Arith<T>::bits_t) +
                        4 /*ki*/ + 4 /*pmask*/ + 4 /*rlist*/ + 2 /*olist*/ +
-                       2 * kMaxCells /*cell entries*/) +
+                       2 * kEntryBudget /*cell entries*/) +
          ((size_t)G * G * G + 1) * 4;
 }
 
@@ -109,8 +110,8 @@ __global__ void __launch_bounds__(NT, 1) fps_grid_kernel(const BucketParams prm,
   uint32_t* pmask = ki + nb;                             // [nb] flagging points of the round
   int32_t* rlist = reinterpret_cast<int32_t*>(pmask + nb);  // [nb] round list
   uint32_t* coff = reinterpret_cast<uint32_t*>(rlist + nb);  // [NC + 1] cell -> end offset
-  uint16_t* cent = reinterpret_cast<uint16_t*>(coff + NC + 1);  // [nb * kMaxCells]
-  uint16_t* olist = cent + (size_t)nb * kMaxCells;              // [nb] oversize buckets
+  uint16_t* cent = reinterpret_cast<uint16_t*>(coff + NC + 1);  // [nb * kEntryBudget]
+  uint16_t* olist = cent + (size_t)nb * kEntryBudget;           // [nb] oversize buckets
   __shared__ bits_t wm_s[NW];
   __shared__ bits_t rv_s[NREC], r2_s[NREC];
   __shared__ uint32_t ri_s[NREC];
@@ -122,7 +123,7 @@ __global__ void __launch_bounds__(NT, 1) fps_grid_kernel(const BucketParams prm,
   __shared__ uint32_t si_w[NW][KM];
   __shared__ int32_t sq_w[NW][KM];
   __shared__ int16_t top_w[NW][KM];
-  __shared__ int ncand_s, rcount_s, ocount_s;
+  __shared__ int ncand_s, rcount_s, ocount_s, ebudget_s;
   __shared__ T glo_s[3], ginv_s[3];
   __shared__ T red_s[2][NW][3];
   __shared__ uint32_t cscr_s[NW][2][32];  // per-warp cell scratch of the flag phase
@@ -159,6 +160,7 @@ __global__ void __launch_bounds__(NT, 1) fps_grid_kernel(const BucketParams prm,
   if (tid == 0) {
     ocount_s = 0;
     rcount_s = 0;
+    ebudget_s = nb * kEntryBudget;
   }
   __syncthreads();
   if (tid < 3) {
@@ -176,7 +178,9 @@ __global__ void __launch_bounds__(NT, 1) fps_grid_kernel(const BucketParams prm,
     const int i = (int)((v - glo[c]) * ginv[c]);
     return i < 0 ? 0 : (i >= G ? G - 1 : i);
   };
-  // register every bucket in the cells its box overlaps (or as oversize)
+  // register every bucket in the cells its box overlaps (<= kMaxCells cells,
+  // within the shared entry budget), the rest as oversize; pmask marks the
+  // registered buckets during the build
   for (int pass = 0; pass < 2; ++pass) {
     for (int q = tid; q < nb; q += NT) {
       int c0[3], c1[3];
@@ -186,8 +190,14 @@ __global__ void __launch_bounds__(NT, 1) fps_grid_kernel(const BucketParams prm,
         c1[c] = cellc(box[q * 6 + 3 + c], c);
       }
       const int cnt = (c1[0] - c0[0] + 1) * (c1[1] - c0[1] + 1) * (c1[2] - c0[2] + 1);
-      if (cnt > kMaxCells) {
-        if (pass == 0) olist[atomicAdd(&ocount_s, 1)] = (uint16_t)q;
+      if (pass == 0) {
+        const bool reg = cnt <= kMaxCells && atomicSub(&ebudget_s, cnt) >= cnt;
+        pmask[q] = reg ? 1u : 0u;
+        if (!reg) {
+          olist[atomicAdd(&ocount_s, 1)] = (uint16_t)q;
+          continue;
+        }
+      } else if (pmask[q] == 0u) {
         continue;
       }
       for (int x = c0[0]; x <= c1[0]; ++x)
@@ -217,6 +227,8 @@ __global__ void __launch_bounds__(NT, 1) fps_grid_kernel(const BucketParams prm,
       __syncthreads();
     }
   }
+  for (int q = tid; q < nb; q += NT) pmask[q] = 0u;
+  __syncthreads();
   // after the fill pass coff[c] = end of cell c (= start of c + 1), start(c) = coff[c - 1]
 
   // ---- seed (fps_core.py:124-130) -----------------------------------------------
@@ -269,6 +281,7 @@ __global__ void __launch_bounds__(NT, 1) fps_grid_kernel(const BucketParams prm,
   int k = 1;
   for (int round = 0; k < iters; ++round) {
     long long t0 = 0, t1 = 0, t2 = 0, t3 = 0;
+    int ntest_w = 0;  // traced: entries tested by this warp
     if (trace) t0 = clock64();
     // A. flag ---------------------------------------------------------------------
     const T r2 = A::from_bits(rmax);
@@ -322,6 +335,7 @@ __global__ void __launch_bounds__(NT, 1) fps_grid_kernel(const BucketParams prm,
             if (lane >= o) incl += u;
           }
           const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+          ntest_w += (int)total;
           cs[lane] = e0;
           ci[lane] = incl;
           __syncwarp();
@@ -563,7 +577,7 @@ __global__ void __launch_bounds__(NT, 1) fps_grid_kernel(const BucketParams prm,
     if (trace && round < prm.trace_iters) {
       long long* rr = trace + (int64_t)round * 8;
       rr[0] = t0; rr[1] = t1; rr[2] = t2; rr[3] = t3; rr[4] = clock64(); rr[5] = acc;
-      rr[6] = nr; rr[7] = full;
+      rr[6] = nr; rr[7] = (long long)full | ((long long)nover << 1) | ((long long)ntest_w << 24);
     }
     k += acc;
   }

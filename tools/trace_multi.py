@@ -47,6 +47,10 @@ def main():
         sl = slice(lo, hi)
         tot = t[0, sl, 4] - t[0, sl, 0]
         flagged = t[0, sl, 6] if a.sched == "grid" else t[:, sl, 6].sum(0)
+        if a.sched == "grid":
+            info = t[0, sl, 7]
+            print(f"   oversize buckets {(info[0] >> 1) & 0x7fffff}, cell entries per point "
+                  f"(warps with a point) {np.mean([((t[w, sl, 7] >> 24) / 2).mean() for w in range(t.shape[0])]):.1f}")
         print(f"rounds [{lo},{hi}): cycles/round median {np.median(tot):.0f}, winners/round "
               f"{nsel[sl].mean():.2f}, flagged/round {flagged.mean():.1f}" +
               (f", full-scan rounds {t[0, sl, 7].mean():.2f}" if a.sched == "grid" else ""))
