@@ -119,8 +119,9 @@ def make_clouds(kind: str, batch: int, n: int, first: int) -> np.ndarray:
 
 # ------------------------------------------------------------------- clocks
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled every 200 ms while the
-    timed region runs (B200_PROFILING.md clocks line)."""
+    """nvidia-smi clocks / throttle reasons sampled every 50 ms while the
+    timed region runs (B200_PROFILING.md clocks line); one query right after
+    the region if it ended before the first sample."""
 
     Q = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
@@ -134,7 +135,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                 "-lms", "200", "-i", str(self.index)],
+                 "-lms", "50", "-i", str(self.index)],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except OSError:
             self.proc = None
@@ -150,6 +151,14 @@ class ClockSampler:
                 self.proc.kill()
                 out, _ = self.proc.communicate()
             self.lines = [ln for ln in out.splitlines() if ln.strip()]
+            if not self.lines:  # region shorter than the first sample: query once now
+                try:
+                    self.lines = [ln for ln in subprocess.run(
+                        ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                         "-i", str(self.index)], capture_output=True, text=True,
+                        timeout=10).stdout.splitlines() if ln.strip()]
+                except (OSError, subprocess.TimeoutExpired):
+                    self.lines = []
         return False
 
     def summary(self) -> dict:

@@ -106,6 +106,7 @@ struct GridInst {
   int dtype;
   int nt;
   int ppl;
+  int km;          // winners per round at most
   const void* fn;  // fps_grid_kernel(BucketParams, int G)
   size_t esz;
 };

@@ -87,7 +87,8 @@ __global__ void __launch_bounds__(NT, 1) fps_grid_kernel(const BucketParams prm,
   constexpr int NREC = 128;
   constexpr int RPL = NREC / 32;
   static_assert(KM <= 32, "one candidate per lane in the chain test");
-  static_assert(NW >= 2 && NW >= KM, "two warps per point, KM warp maxima");
+  static_assert(NW >= KM, "KM warp maxima, at least one warp per point");
+  constexpr int WPP = NW / KM >= 2 ? 2 : 1;  // warps per selected point in the flag phase
 
   const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nb = (int)prm.nbuckets;
@@ -304,8 +305,8 @@ __global__ void __launch_bounds__(NT, 1) fps_grid_kernel(const BucketParams prm,
       // point's cube are spread over the 64 lanes: per chunk of 32 cells the
       // warp publishes each cell's first entry and inclusive entry count in
       // shared scratch, then every lane walks flat entry indices
-      for (int t = warp >> 1; t < J; t += NW / 2) {
-        const int half = warp & 1;
+      for (int t = warp / WPP; t < J; t += NW / WPP) {
+        const int half = warp % WPP;
         const T px = sp_w[warp][t][0], py = sp_w[warp][t][1], pz = sp_w[warp][t][2];
         const T pad = (fabs(px) + fabs(py) + fabs(pz) + T(1)) * T(1e-6);
         int c0[3], c1[3];
@@ -339,7 +340,7 @@ __global__ void __launch_bounds__(NT, 1) fps_grid_kernel(const BucketParams prm,
           cs[lane] = e0;
           ci[lane] = incl;
           __syncwarp();
-          for (uint32_t f0 = 32 * half; f0 < total; f0 += 64) {  // uniform trip count
+          for (uint32_t f0 = 32 * half; f0 < total; f0 += 32 * WPP) {  // uniform trip count
             const uint32_t f = f0 + lane;
             int q = 0;
             if (f < total) {
@@ -356,7 +357,7 @@ __global__ void __launch_bounds__(NT, 1) fps_grid_kernel(const BucketParams prm,
           }
           __syncwarp();
         }
-        for (int i0 = 32 * half; i0 < nover; i0 += 64) {
+        for (int i0 = 32 * half; i0 < nover; i0 += 32 * WPP) {
           const int i = i0 + lane;
           test_warp(i < nover, i < nover ? olist[i] : 0, t, px, py, pz);
         }
@@ -596,6 +597,7 @@ GridInst make_ginst() {
   k.dtype = sizeof(T) == 4 ? 0 : 1;
   k.nt = kBucketThreads;
   k.ppl = PPL;
+  k.km = KM;
   k.fn = reinterpret_cast<const void*>(&fps_grid_kernel<T, kBucketThreads, PPL, KM>);
   k.esz = sizeof(T);
   return k;

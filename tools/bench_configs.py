@@ -47,10 +47,10 @@ def main():
             if kind == "lidar" and N < 100000:
                 continue
             x = torch.from_numpy(bench.make_clouds(kind, B, N, 0)).cuda()
-            for sched in ("bucket", "stream"):
+            for sched in ("auto", "bucket", "grid", "stream"):
                 prev = _device.set_schedule(sched)
                 try:
-                    heavy = N >= 100000 and sched == "stream"
+                    heavy = N >= 100000 and sched in ("stream", "bucket")
                     ex = timeit(lambda: ffps.hierarchical_sample_batch(
                         x, budgets, ffps.PruneConfig(p=0.0), 0, False),
                         1 if heavy else 2, 3 if heavy else 5)
