@@ -217,6 +217,21 @@ def main():
         add({"op": "coverage", "cloud": cl, "sample": how,
              "value": ref.coverage_radius(idx, cloud)}, sample=idx)
 
+    # ---- FPSC v1 cache wire format (fps_cache.py:26-33, :82-116), reference bytes
+    for t, (kind, n, m1, p) in enumerate((("uniform", 200, 50, 0.4), ("ties", 64, 20, 0.0),
+                                          ("uniform32", 1000, 250, 0.75))):
+        pts, cl = cloud_entry(kind, n, 7000 + t)
+        cloud = ref.PointCloud(pts)
+        sample, _ = ref.fps_prune(cloud, m1, ref.PruneConfig(p=p), 0)
+        cache = ref.CacheRecord.from_sample(cloud, sample)
+        blob = cache.to_bytes()
+        back = ref.CacheRecord.from_bytes(blob)
+        add({"op": "fpsc", "cloud": cl, "m1": m1, "p": p, "fill_boundary": sample.fill_boundary,
+             "back_fill_boundary": back.layer1.fill_boundary,
+             "footprint": cache.footprint_bytes},
+            indices=sample.indices, sel=sample.selection_dist2,
+            blob=np.frombuffer(blob, dtype=np.uint8))
+
     np.savez_compressed(os.path.join(HERE, "golden.npz"), **arrays)
     meta = {"numpy": np.__version__, "reference": "/root/reference/pkg (flashfps "
             f"{ref.__version__})", "cases": cases}
