@@ -448,8 +448,10 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     kms = float(np.mean([k[3] for k in kern])) if kern else float("nan")
     pk = peaks()
     achieved = units_launch * BYTES_PER_UNIT_F32 / (kms / 1e3) / 1e9
-    sched = _native.auto_schedule(c1, B)
-    plan = {"schedule": sched, **_native.bucket_plan(_native.F32, c1)} \
+    sched_full = _native.auto_schedule(c1, B)   # e.g. "grid@2" = K1g, 2 CTAs per cloud
+    sched = sched_full.split("@")[0]
+    plan = {"schedule": sched, "schedule_auto": sched_full,
+            **_native.bucket_plan(_native.F32, c1)} \
         if sched in ("bucket", "multi", "grid") else \
         {"schedule": "stream", **_native.plan(_native.F32, c1, B)}
     sm_mhz = clocks["sm_mhz"] or pk["sm_max_mhz"]

@@ -85,11 +85,16 @@ int ffps_run_kernel(int dtype, const void* xyz, int64_t batch,
  *                     the top candidates provably unaffected by each other);
  *   FFPS_ALGO_GRID    K0 + K1g: MULTI with the buckets indexed by a cell grid, so
  *                     a selected point only tests the buckets within its reach;
- *   FFPS_ALGO_AUTO    GRID for n >= 65536; BUCKET for n >= 2048 and batch >= 48;
- *                     else STREAM (the environment variable
+ *                     each cloud's buckets are split over a cluster of 1, 2 or
+ *                     4 CTAs: FFPS_ALGO_GRID_CL(c) fixes c, plain FFPS_ALGO_GRID
+ *                     picks the largest c with batch * c <= SM count;
+ *   FFPS_ALGO_AUTO    GRID for n >= 65536 (any batch) or n >= 24576 with >= 16
+ *                     clouds; BUCKET for mid-size clouds when the batch fills
+ *                     the GPU; else STREAM (the environment variable
  *                     FFPS_ALGO=stream|bucket|multi|grid overrides AUTO). */
 enum ffps_algo { FFPS_ALGO_AUTO = 0, FFPS_ALGO_STREAM = 1, FFPS_ALGO_BUCKET = 2,
                  FFPS_ALGO_MULTI = 3, FFPS_ALGO_GRID = 4 };
+#define FFPS_ALGO_GRID_CL(c) (FFPS_ALGO_GRID | ((c) << 8))
 
 /* Host -> device copy of the candidate prefix xyz[b][0:n_prefix) of every
  * cloud (the only coordinates a cache-on FlashFPS run reads,
@@ -100,8 +105,9 @@ int ffps_h2d_prefix(void* dst, const void* src_host, int64_t batch, int64_t n_pr
                     int64_t cloud_stride, int dtype, void* stream);
 
 /* The schedule FFPS_ALGO_AUTO picks for a batch of `batch` clouds of n points
- * (FFPS_ALGO_STREAM or FFPS_ALGO_BUCKET); callers that split one batch into
- * chunks decide once for the whole batch. */
+ * (FFPS_ALGO_STREAM, FFPS_ALGO_BUCKET or FFPS_ALGO_GRID_CL(c) with the
+ * cluster size chosen for the whole batch); callers that split one batch into
+ * concurrent chunks decide once for the whole batch and pass the result. */
 int ffps_auto_schedule(int64_t n, int64_t batch);
 
 /* ffps_run_kernel with an explicit schedule (same arguments; algo as above). */

@@ -19,7 +19,9 @@ LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib",
                         "libflashfps_b200.so")
 
 F32, F64 = 0, 1
-ALGO = {"auto": 0, "stream": 1, "bucket": 2, "multi": 3, "grid": 4}
+ALGO = {"auto": 0, "stream": 1, "bucket": 2, "multi": 3, "grid": 4,
+        # K1g with a fixed number of CTAs per cloud (FFPS_ALGO_GRID_CL(c))
+        "grid@1": 4 | 1 << 8, "grid@2": 4 | 2 << 8, "grid@4": 4 | 4 << 8}
 _STATUS = {-1: "EINVAL", -2: "EUNSUPPORTED", -3: "ECUDA"}
 
 _lock = threading.Lock()
@@ -114,8 +116,10 @@ def bucket_plan(dtype: int, n: int) -> dict:
 
 
 def auto_schedule(n: int, batch: int) -> str:
-    """The schedule AUTO picks for a whole batch ("stream" or "bucket")."""
-    return {1: "stream", 2: "bucket", 3: "multi", 4: "grid"}[int(load().ffps_auto_schedule(n, batch))]
+    """The schedule AUTO picks for a whole batch ("stream", "bucket" or
+    "grid@c", c = CTAs per cloud chosen for the whole batch)."""
+    names = {v: k for k, v in ALGO.items()}
+    return names[int(load().ffps_auto_schedule(n, batch))]
 
 
 def h2d_prefix(dst, src_host, batch, n_prefix, cloud_stride, dtype, stream) -> None:

@@ -385,26 +385,30 @@ int run_bucketed(int dtype, const void* xyz, int64_t batch, int64_t cloud_stride
 }
 
 // K1g: smallest bucket size whose bucket table + cell index fit shared memory
+int grid_cluster(int algo, int64_t batch, int sms);
+
 int run_grid(int dtype, const void* xyz, int64_t batch, int64_t cloud_stride, int64_t n,
              int64_t iters, const int64_t* seed_pos, const int64_t* index_map, int64_t map_stride,
-             int64_t* order, void* sel_d2, int64_t out_stride, cudaStream_t st, int dev) {
+             int64_t* order, void* sel_d2, int64_t out_stride, cudaStream_t st, int dev,
+             int algo) {
   const DeviceInfo di = device_info(dev);
   int cnt = 0;
   const ffps::GridInst* insts = ffps::grid_instances(&cnt);
   const ffps::GridInst* pick = nullptr;
   const int km = 8;  // winners per round (KM = 16 measured 1.3-1.6x slower)
+  const int cl = grid_cluster(algo, batch, di.sms);  // CTAs per cloud
   int64_t nb = 0;
-  int G = 4;
   size_t smem = 0;
   for (int ppl = 1; ppl <= 8 && !pick; ppl *= 2) {
     nb = (n + 32 * ppl - 1) / (32 * ppl);
-    if (nb > 65535) continue;
-    G = (int)std::lround(std::cbrt((double)nb / 2.0));
-    G = G < 4 ? 4 : (G > 16 ? 16 : G);
-    smem = ffps::grid_smem(dtype, nb, G);
-    if (smem + 16384 > di.smem_optin) continue;  // + static shared memory
+    const int64_t nbl = (nb + cl - 1) / cl;  // buckets of cluster rank 0 (the most)
+    if (nbl > 4096) continue;                 // <= 128 bucket groups per CTA
+    smem = ffps::grid_smem(dtype, nbl);
+    if (smem + 20480 > di.smem_optin) continue;  // + static shared memory
     for (int i = 0; i < cnt; ++i)
-      if (insts[i].dtype == dtype && insts[i].ppl == ppl && insts[i].km == km) pick = &insts[i];
+      if (insts[i].dtype == dtype && insts[i].ppl == ppl && insts[i].km == km &&
+          insts[i].cl == cl)
+        pick = &insts[i];
   }
   if (!pick) return fail(FFPS_EUNSUPPORTED, "no grid configuration for n=%lld", (long long)n);
   const int64_t bs = 32 * pick->ppl;
@@ -488,8 +492,22 @@ int run_grid(int dtype, const void* xyz, int64_t batch, int64_t cloud_stride, in
       g_attr_done[key] = true;
     }
   }
-  void* args[] = {&prm, &G};
-  e = cudaLaunchKernel(pick->fn, dim3((unsigned)batch), dim3(pick->nt), args, smem, st);
+  void* args[] = {&prm};
+  {
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = dim3((unsigned)(batch * pick->cl));
+    lc.blockDim = dim3(pick->nt);
+    lc.dynamicSmemBytes = smem;
+    lc.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = (unsigned)pick->cl;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    e = cudaLaunchKernelExC(&lc, pick->fn, args);
+  }
   if (e != cudaSuccess) {
     cudaFreeAsync(scratch, st);
     return cuda_fail(e, "fps_grid_kernel launch");
@@ -571,15 +589,22 @@ int run_streaming(int dtype, const void* xyz, int64_t batch, int64_t cloud_strid
   return FFPS_OK;
 }
 
-// FFPS_ALGO_AUTO (measured on B200, tools/sweep_schedules.sh,
-// profiles/r01_schedules.jsonl): GRID (multi-winner rounds + cell index) for
-// clouds of >= 64K points at any batch; BUCKET when the batch alone fills the
-// GPU (>= 48 clouds of >= 2048 points); STREAM otherwise (few small clouds:
-// the cluster kernel spreads each cloud over many SMs).  FFPS_ALGO in the
-// environment ("stream" / "bucket" / "multi" / "grid") overrides AUTO.
-constexpr int64_t kAutoBucketMin = 2048;
-constexpr int64_t kAutoBucketBatch = 48;
-constexpr int64_t kAutoGridMin = 65536;
+// FFPS_ALGO_AUTO (measured on B200 over batch 1..128 x n 4K..128K with
+// iters = n/4, tools/sweep_auto.py, profiles/r01_sweep_auto.jsonl):
+//   GRID   (multi-winner rounds, cell index, 1-4 CTAs per cloud) for clouds of
+//          >= 64K points at any batch, and >= 24K points once >= 16 clouds;
+//   BUCKET (one CTA per cloud, exact bucket bounds) for mid-size clouds when the
+//          batch fills the GPU (>= 16 clouds of >= 12K points, >= 48 of >= 6K,
+//          >= 96 of >= 3K);
+//   STREAM (clusters of up to 16 CTAs, every point every iteration) otherwise.
+// FFPS_ALGO in the environment ("stream" / "bucket" / "multi" / "grid")
+// overrides AUTO.
+int auto_algo(int64_t n, int64_t batch) {
+  if (n >= 65536 || (n >= 24576 && batch >= 16)) return FFPS_ALGO_GRID;
+  if ((n >= 12288 && batch >= 16) || (n >= 6144 && batch >= 48) || (n >= 3072 && batch >= 96))
+    return FFPS_ALGO_BUCKET;
+  return FFPS_ALGO_STREAM;
+}
 
 int resolve_algo(int algo, int64_t n, int64_t batch) {
   if (algo == FFPS_ALGO_AUTO) {
@@ -590,11 +615,25 @@ int resolve_algo(int algo, int64_t n, int64_t batch) {
     if (env && strcmp(env, "bucket") == 0) return FFPS_ALGO_BUCKET;
     if (env && strcmp(env, "multi") == 0) return FFPS_ALGO_MULTI;
     if (env && strcmp(env, "grid") == 0) return FFPS_ALGO_GRID;
-    if (n >= kAutoGridMin) return FFPS_ALGO_GRID;
-    return n >= kAutoBucketMin && batch >= kAutoBucketBatch ? FFPS_ALGO_BUCKET
-                                                            : FFPS_ALGO_STREAM;
+    return auto_algo(n, batch);
   }
   return algo;
+}
+
+// CTAs per cloud of the grid schedule: fixed by the algo argument
+// (FFPS_ALGO_GRID_CL), else the largest of 1/2/4 with batch * c <= SMs;
+// FFPS_GRID_CL in the environment overrides both
+int grid_cluster(int algo, int64_t batch, int sms) {
+  int cl = algo >> 8;
+  if (cl == 0) {
+    cl = 1;
+    while (cl < 4 && batch * (cl * 2) <= sms) cl *= 2;
+  }
+  if (const char* v = getenv("FFPS_GRID_CL")) {
+    const int w = atoi(v);
+    if (w == 1 || w == 2 || w == 4) cl = w;
+  }
+  return cl;
 }
 
 }  // namespace
@@ -635,7 +674,14 @@ int ffps_h2d_prefix(void* dst, const void* src_host, int64_t batch, int64_t n_pr
 }
 
 int ffps_auto_schedule(int64_t n, int64_t batch) {
-  return resolve_algo(FFPS_ALGO_AUTO, n, batch);
+  const int a = resolve_algo(FFPS_ALGO_AUTO, n, batch);
+  if (a != FFPS_ALGO_GRID) return a;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) {
+    cudaGetLastError();
+    return a;
+  }
+  return FFPS_ALGO_GRID_CL(grid_cluster(a, batch, device_info(dev).sms));
 }
 
 int ffps_run_kernel_ex(int dtype, const void* xyz, int64_t batch, int64_t cloud_stride,
@@ -646,7 +692,8 @@ int ffps_run_kernel_ex(int dtype, const void* xyz, int64_t batch, int64_t cloud_
   if (dtype != FFPS_F32 && dtype != FFPS_F64)
     return fail(FFPS_EINVAL, "dtype must be FFPS_F32 or FFPS_F64");
   if (algo != FFPS_ALGO_AUTO && algo != FFPS_ALGO_STREAM && algo != FFPS_ALGO_BUCKET &&
-      algo != FFPS_ALGO_MULTI && algo != FFPS_ALGO_GRID)
+      algo != FFPS_ALGO_MULTI && algo != FFPS_ALGO_GRID && algo != FFPS_ALGO_GRID_CL(1) &&
+      algo != FFPS_ALGO_GRID_CL(2) && algo != FFPS_ALGO_GRID_CL(4))
     return fail(FFPS_EINVAL, "unknown algorithm %d", algo);
   if (batch < 0) return fail(FFPS_EINVAL, "batch=%lld < 0", (long long)batch);
   if (batch == 0) return FFPS_OK;
@@ -663,9 +710,9 @@ int ffps_run_kernel_ex(int dtype, const void* xyz, int64_t batch, int64_t cloud_
   if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int a = resolve_algo(algo, n, batch);
-  if (a == FFPS_ALGO_GRID)
+  if ((a & 0xff) == FFPS_ALGO_GRID)
     return run_grid(dtype, xyz, batch, cloud_stride, n, iters, seed_pos, index_map, map_stride,
-                    order, sel_d2, out_stride, st, dev);
+                    order, sel_d2, out_stride, st, dev, a);
   if (a == FFPS_ALGO_BUCKET || a == FFPS_ALGO_MULTI)
     return run_bucketed(dtype, xyz, batch, cloud_stride, n, iters, seed_pos, index_map,
                         map_stride, order, sel_d2, out_stride, st, dev, a == FFPS_ALGO_MULTI);
@@ -704,8 +751,9 @@ int ffps_coverage(int dtype, const void* xyz, int64_t batch, int64_t cloud_strid
   const int64_t bsp = 32;
   const int64_t nbp = (n + bsp - 1) / bsp, nbs = (m + bss - 1) / bss;
   const int64_t nsp = nbp * bsp, nss = nbs * bss;
-  const size_t per_p = (size_t)nsp * (4 * esz + 4) + (size_t)nbp * 6 * esz;
-  const size_t per_s = (size_t)nss * (4 * esz + 4) + (size_t)nbs * 6 * esz;
+  // per slot: X, Y, Z, D + O, and the K0 scratch TX, TY, TZ + TO
+  const size_t per_p = (size_t)nsp * (7 * esz + 8) + (size_t)nbp * 6 * esz;
+  const size_t per_s = (size_t)nss * (7 * esz + 8) + (size_t)nbs * 6 * esz;
   unsigned char* scratch = nullptr;
   e = cudaMallocAsync(reinterpret_cast<void**>(&scratch), (per_p + per_s) * (size_t)batch + 512,
                       st);
@@ -722,8 +770,11 @@ int ffps_coverage(int dtype, const void* xyz, int64_t batch, int64_t cloud_strid
     bb.nslots = nslots;
     bb.nbuckets = nb;
     bb.bs = bs;
-    bb.TX = bb.TY = bb.TZ = nullptr;
-    bb.TO = nullptr;
+    unsigned char* t = reinterpret_cast<unsigned char*>(bb.O) + (size_t)nslots * 4 * (size_t)batch;
+    bb.TX = t;
+    bb.TY = t + arr;
+    bb.TZ = t + 2 * arr;
+    bb.TO = reinterpret_cast<int32_t*>(t + 3 * arr);
   };
   ffps::BucketBuildParams bp{}, bs{};
   bp.xyz = xyz;

@@ -18,6 +18,8 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
+#include <cstring>
 
 #include "ffps_internal.h"
 
@@ -333,6 +335,11 @@ size_t bucket_build_smem() {
 
 cudaError_t launch_bucket_build(int dtype, const BucketBuildParams& p, int64_t batch,
                                 cudaStream_t st) {
+  // default: kd-tree leaves (bucket_kd.cu; needs the TX..TO scratch);
+  // FFPS_BUCKET_BUILD=morton selects the Morton-grid build below
+  const char* kind = getenv("FFPS_BUCKET_BUILD");
+  if (p.TX != nullptr && !(kind && strcmp(kind, "morton") == 0))
+    return launch_bucket_kd(dtype, p, batch, st);
   const void* fn = dtype == 0 ? reinterpret_cast<const void*>(&bucket_build_kernel<float>)
                               : reinterpret_cast<const void*>(&bucket_build_kernel<double>);
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -1,0 +1,562 @@
+// K0-kd — kd-tree bucketing of the point set of every cloud (default K0).
+//
+// Same output contract as the Morton K0 (bucket_build.cu): bucket-major SoA
+// X, Y, Z, D, O [nb * BS] and boxes BB [nb][6]; padding slots (>= n) repeat
+// the first point of the last bucket with D = -inf, O = -1.
+//
+// Buckets are the leaves of a kd-tree: a segment of m > BS points is split on
+// the longest axis of its box so that the left child holds nl =
+// ((m / BS + 1) / 2) * BS points (a whole number of buckets: every segment
+// starts on a bucket boundary and only the rightmost leaf — the last bucket —
+// can be partial).  The split value is located with a 1024-bin histogram of
+// the segment along that axis; the boundary bin is divided by arrival order.
+// A leaf's box is then as compact as 32 * PPL points allow, whatever the
+// density: on LiDAR frames (1/r^2 density, scan rings) the Morton buckets of
+// a fixed grid span up to ~7 m while kd leaves stay near the local spacing,
+// and the greedy kernels flag ~4x (uniform ~2x) fewer buckets per selected
+// point (SIMULATED and measured, K0).
+//
+// One CTA (1024 threads) per cloud; points ping-pong between the output
+// arrays (X, Y, Z, O) and the scratch arrays (TX, TY, TZ, TO):
+//   CTA phase  level-synchronous while there are < 32 segments: histogram
+//              pass, per-segment scan (one warp each), partition pass with
+//              warp-aggregated shared-memory counters; children boxes are
+//              accumulated during the partition (no separate box pass);
+//   warp phase each warp splits its segment(s) depth-first down to the
+//              leaves with an explicit stack, counters in registers.
+// Leaves that end in the scratch arrays are copied back.  Like the Morton
+// build, the slot order inside a bucket depends on arrival order; the greedy
+// kernels break ties by position O, never by slot, so results are unchanged.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "ffps_internal.h"
+
+namespace ffps {
+
+namespace {
+
+constexpr int kThreads = 1024;
+constexpr int kNW = kThreads / 32;
+constexpr int kBins = 1024;
+constexpr int kMaxSeg = kNW;   // CTA phase stops at this many segments
+constexpr int kStack = 24;     // per-warp DFS stack (depth <= log2(n / BS) + 1)
+
+// order-preserving integer image of a float / double (for shared atomics)
+template <typename T>
+struct Ord;
+template <>
+struct Ord<float> {
+  using I = int;
+  __device__ static I enc(float f) {
+    const int b = __float_as_int(f);
+    return b >= 0 ? b : b ^ 0x7fffffff;
+  }
+  __device__ static float dec(I i) { return __int_as_float(i >= 0 ? i : i ^ 0x7fffffff); }
+  static constexpr I kMax = 0x7fffffff;
+  static constexpr I kMin = (int)0x80000000;
+};
+template <>
+struct Ord<double> {
+  using I = long long;
+  __device__ static I enc(double f) {
+    const long long b = __double_as_longlong(f);
+    return b >= 0 ? b : b ^ 0x7fffffffffffffffLL;
+  }
+  __device__ static double dec(I i) {
+    return __longlong_as_double(i >= 0 ? i : i ^ 0x7fffffffffffffffLL);
+  }
+  static constexpr I kMax = 0x7fffffffffffffffLL;
+  static constexpr I kMin = (long long)0x8000000000000000ULL;
+};
+
+template <typename T>
+__device__ __forceinline__ T wmin(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const T u = __shfl_xor_sync(0xffffffffu, v, o);
+    v = u < v ? u : v;
+  }
+  return v;
+}
+template <typename T>
+__device__ __forceinline__ T wmax(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const T u = __shfl_xor_sync(0xffffffffu, v, o);
+    v = u > v ? u : v;
+  }
+  return v;
+}
+
+template <typename T>
+__device__ __forceinline__ int bin_of(T v, T lo, T inv) {
+  const int c = (int)((v - lo) * inv);
+  return c < 0 ? 0 : (c >= kBins ? kBins - 1 : c);
+}
+
+// split of a segment: nl points (a multiple of bs) to the left child
+__device__ __forceinline__ int left_size(int m, int bs) { return ((m / bs + 1) / 2) * bs; }
+
+// warp: locate the boundary bin of rank nl in a 1024-bin histogram h
+// (lane owns bins [32 * lane, 32 * lane + 32)); returns bin, count before it
+// and the bin's own count (uniform across the warp)
+__device__ __forceinline__ void find_split(const uint32_t* h, int nl, int lane, int& bstar,
+                                           int& before, int& mid) {
+  uint32_t loc = 0;
+#pragma unroll 8
+  for (int j = 0; j < 32; ++j) loc += h[lane * 32 + j];
+  uint32_t incl = loc;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t u = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += u;
+  }
+  const unsigned hit = __ballot_sync(0xffffffffu, incl >= (uint32_t)nl);
+  const int L = __ffs(hit) - 1;  // nl <= m - 1 < total, so some lane hits
+  int b = 0, bef = 0, c = 0;
+  if (lane == L) {
+    uint32_t run = incl - loc;
+    for (int j = 0; j < 32; ++j) {
+      const uint32_t v = h[lane * 32 + j];
+      if (run + v >= (uint32_t)nl) {
+        b = lane * 32 + j;
+        bef = (int)run;
+        c = (int)v;
+        break;
+      }
+      run += v;
+    }
+  }
+  bstar = __shfl_sync(0xffffffffu, b, L);
+  before = __shfl_sync(0xffffffffu, bef, L);
+  mid = __shfl_sync(0xffffffffu, c, L);
+}
+
+template <typename T>
+struct Bufs {
+  T *x, *y, *z;
+  int32_t* o;
+};
+
+}  // namespace
+
+template <typename T>
+__global__ void __launch_bounds__(kThreads, 1) bucket_kd_kernel(const BucketBuildParams p) {
+  using O = Ord<T>;
+  using I = typename O::I;
+  extern __shared__ __align__(16) uint32_t hist[];  // [kMaxSeg][kBins] / [kNW][kBins], stack boxes
+  __shared__ int s_start[kMaxSeg], s_m[kMaxSeg], s_nl[kMaxSeg], s_ax[kMaxSeg];
+  __shared__ int s_b[kMaxSeg], s_lt[kMaxSeg], s_take[kMaxSeg], s_mid[kMaxSeg];
+  __shared__ int s_cl[kMaxSeg], s_cm[kMaxSeg], s_cr[kMaxSeg];
+  __shared__ T s_lo[kMaxSeg], s_inv[kMaxSeg];
+  __shared__ I s_box[kMaxSeg][6];       // boxes of the current segments
+  __shared__ I s_cbox[2 * kMaxSeg][6];  // boxes of their children
+  __shared__ int s_S;
+  // warp phase stack
+  __shared__ int w_start[kNW][kStack], w_m[kNW][kStack], w_par[kNW][kStack];
+  T(*w_box)[kStack][6] = reinterpret_cast<T(*)[kStack][6]>(hist + kMaxSeg * kBins);
+
+  const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int n = (int)p.n;
+  const int bs = (int)p.bs;
+  const T* X0 = static_cast<const T*>(p.xyz) + (int64_t)b * p.cloud_stride * 3;
+  const int64_t* map = p.index_map ? p.index_map + (int64_t)b * p.map_stride : nullptr;
+  const int64_t base = (int64_t)b * p.nslots;
+  const Bufs<T> out{static_cast<T*>(p.X) + base, static_cast<T*>(p.Y) + base,
+                   static_cast<T*>(p.Z) + base, p.O + base};
+  const Bufs<T> tmp{static_cast<T*>(p.TX) + base, static_cast<T*>(p.TY) + base,
+                    static_cast<T*>(p.TZ) + base, p.TO + base};
+  auto buf = [&](int pr) { return pr ? tmp : out; };
+  T* D = static_cast<T*>(p.D) + base;
+  T* BB = static_cast<T*>(p.BB) + (int64_t)b * p.nbuckets * 6;
+  const T pinf = (T)INFINITY;
+
+  // 0. gather the run's points into buf[0] (position order) + cloud box
+  if (tid < 6) s_box[0][tid] = tid < 3 ? O::kMax : O::kMin;
+  __syncthreads();
+  {
+    T a[3] = {pinf, pinf, pinf}, z[3] = {-pinf, -pinf, -pinf};
+    for (int i = tid; i < n; i += kThreads) {
+      const int64_t s = map ? __ldg(map + i) : i;
+      const T v[3] = {X0[3 * s + 0], X0[3 * s + 1], X0[3 * s + 2]};
+      out.x[i] = v[0];
+      out.y[i] = v[1];
+      out.z[i] = v[2];
+      out.o[i] = i;
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        a[c] = v[c] < a[c] ? v[c] : a[c];
+        z[c] = v[c] > z[c] ? v[c] : z[c];
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      a[c] = wmin(a[c]);
+      z[c] = wmax(z[c]);
+    }
+    if (lane == 0) {
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        atomicMin(&s_box[0][c], O::enc(a[c]));
+        atomicMax(&s_box[0][3 + c], O::enc(z[c]));
+      }
+    }
+  }
+  if (tid == 0) {
+    s_S = 1;
+    s_start[0] = 0;
+    s_m[0] = n;
+  }
+  __syncthreads();
+
+  // 1. CTA phase: level-synchronous splits while there are few segments
+  int par = 0;
+  for (;;) {
+    const int S = s_S;
+    bool any = false;
+    for (int s = 0; s < S; ++s) any |= s_m[s] > bs;
+    if (!any || 2 * S > kMaxSeg) break;
+    const Bufs<T> src = buf(par), dst = buf(par ^ 1);
+    // per-segment split parameters; clear histograms and counters
+    if (tid < S) {
+      const int s = tid;
+      T ext[3];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) ext[c] = O::dec(s_box[s][3 + c]) - O::dec(s_box[s][c]);
+      const int ax = ext[0] >= ext[1] ? (ext[0] >= ext[2] ? 0 : 2) : (ext[1] >= ext[2] ? 1 : 2);
+      s_ax[s] = ax;
+      s_lo[s] = O::dec(s_box[s][ax]);
+      s_inv[s] = ext[ax] > (T)0 ? (T)kBins / ext[ax] : (T)0;
+      s_nl[s] = s_m[s] > bs ? left_size(s_m[s], bs) : s_m[s];
+      s_cl[s] = s_cm[s] = s_cr[s] = 0;
+    }
+    if (tid < 2 * S * 6) {
+      const int c = tid % 6;
+      s_cbox[tid / 6][c] = c < 3 ? O::kMax : O::kMin;
+    }
+    for (int i = tid; i < S * kBins; i += kThreads) hist[i] = 0u;
+    __syncthreads();
+    // histogram pass (segment-major: the whole CTA on one segment at a time)
+    for (int s = 0; s < S; ++s) {
+      if (s_m[s] <= bs) continue;
+      const int st = s_start[s], m = s_m[s], ax = s_ax[s];
+      const T lo = s_lo[s], inv = s_inv[s];
+      const T* v = ax == 0 ? src.x : (ax == 1 ? src.y : src.z);
+      uint32_t* h = hist + s * kBins;
+      for (int i = tid; i < m; i += kThreads) atomicAdd(&h[bin_of(v[st + i], lo, inv)], 1u);
+    }
+    __syncthreads();
+    if (warp < S && s_m[warp] > bs) {
+      int bstar, before, mid;
+      find_split(hist + warp * kBins, s_nl[warp], lane, bstar, before, mid);
+      if (lane == 0) {
+        s_b[warp] = bstar;
+        s_lt[warp] = before;
+        s_mid[warp] = mid;
+        s_take[warp] = s_nl[warp] - before;
+      }
+    }
+    __syncthreads();
+    // partition pass + children boxes
+    for (int s = 0; s < S; ++s) {
+      const int st = s_start[s], m = s_m[s];
+      const bool split = m > bs;
+      const int ax = s_ax[s], bstar = split ? s_b[s] : 0;
+      const T lo = s_lo[s], inv = s_inv[s];
+      const int nl = s_nl[s], lt = split ? s_lt[s] : 0, take = split ? s_take[s] : 0;
+      const int midc = split ? s_mid[s] : 0;
+      T a[2][3], z[2][3];
+#pragma unroll
+      for (int k = 0; k < 2; ++k)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          a[k][c] = pinf;
+          z[k][c] = -pinf;
+        }
+      for (int i0 = 0; i0 < m; i0 += kThreads) {  // warp-uniform trip count
+        const int i = i0 + tid;
+        const bool live = i < m;
+        T v[3] = {T(0), T(0), T(0)};
+        int32_t o = 0;
+        int cat = 3;  // 0 left, 1 boundary bin, 2 right
+        if (live) {
+          v[0] = src.x[st + i];
+          v[1] = src.y[st + i];
+          v[2] = src.z[st + i];
+          o = src.o[st + i];
+          if (split) {
+            const int bn = bin_of(v[ax], lo, inv);
+            cat = bn < bstar ? 0 : (bn == bstar ? 1 : 2);
+          } else {
+            cat = 0;
+          }
+        }
+        int pos = 0;
+        if (split) {
+#pragma unroll
+          for (int k = 0; k < 3; ++k) {
+            const unsigned mk = __ballot_sync(0xffffffffu, cat == k);
+            if (!mk) continue;
+            const int ldr = __ffs(mk) - 1;
+            int basek = 0;
+            if (lane == ldr) basek = atomicAdd(k == 0 ? &s_cl[s] : (k == 1 ? &s_cm[s] : &s_cr[s]), __popc(mk));
+            basek = __shfl_sync(0xffffffffu, basek, ldr);
+            if (cat == k) {
+              const int t = basek + __popc(mk & ((1u << lane) - 1u));
+              if (k == 0) pos = t;
+              else if (k == 1) pos = t < take ? lt + t : nl + (t - take);
+              else pos = nl + (midc - take) + t;
+            }
+          }
+        } else {
+          pos = i;
+        }
+        if (live) {
+          dst.x[st + pos] = v[0];
+          dst.y[st + pos] = v[1];
+          dst.z[st + pos] = v[2];
+          dst.o[st + pos] = o;
+          const int k = pos < nl ? 0 : 1;
+#pragma unroll
+          for (int c = 0; c < 3; ++c) {
+            a[k][c] = v[c] < a[k][c] ? v[c] : a[k][c];
+            z[k][c] = v[c] > z[k][c] ? v[c] : z[k][c];
+          }
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < 2; ++k)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          const T mn = wmin(a[k][c]), mx = wmax(z[k][c]);
+          if (lane == 0 && mn <= mx) {
+            atomicMin(&s_cbox[2 * s + k][c], O::enc(mn));
+            atomicMax(&s_cbox[2 * s + k][3 + c], O::enc(mx));
+          }
+        }
+    }
+    __syncthreads();
+    // next level's segment list (children in order; unsplit segments carried)
+    if (tid == 0) {
+      int ns = 0;
+      int st2[kMaxSeg], m2[kMaxSeg], from[kMaxSeg];
+      for (int s = 0; s < S; ++s) {
+        if (s_m[s] > bs) {
+          st2[ns] = s_start[s];
+          m2[ns] = s_nl[s];
+          from[ns++] = 2 * s;
+          st2[ns] = s_start[s] + s_nl[s];
+          m2[ns] = s_m[s] - s_nl[s];
+          from[ns++] = 2 * s + 1;
+        } else {
+          st2[ns] = s_start[s];
+          m2[ns] = s_m[s];
+          from[ns++] = 2 * s;
+        }
+      }
+      for (int s = 0; s < ns; ++s) {
+        s_start[s] = st2[s];
+        s_m[s] = m2[s];
+#pragma unroll
+        for (int c = 0; c < 6; ++c) s_box[s][c] = s_cbox[from[s]][c];
+      }
+      s_S = ns;
+    }
+    par ^= 1;
+    __syncthreads();
+  }
+
+  // 2. warp phase: depth-first splits of each remaining segment
+  {
+    uint32_t* h = hist + warp * kBins;
+    const int S = s_S;
+    for (int s0 = warp; s0 < S; s0 += kNW) {
+      int top = 0;
+      if (lane == 0) {
+        w_start[warp][0] = s_start[s0];
+        w_m[warp][0] = s_m[s0];
+        w_par[warp][0] = par;
+#pragma unroll
+        for (int c = 0; c < 6; ++c) w_box[warp][0][c] = O::dec(s_box[s0][c]);
+      }
+      top = 1;
+      __syncwarp();
+      while (top > 0) {
+        --top;
+        const int st = w_start[warp][top], m = w_m[warp][top], pr = w_par[warp][top];
+        T bx[6];
+#pragma unroll
+        for (int c = 0; c < 6; ++c) bx[c] = w_box[warp][top][c];
+        __syncwarp();
+        const Bufs<T> src = buf(pr), dst = buf(pr ^ 1);
+        if (m <= bs) {  // leaf: must end in the output arrays
+          if (pr == 1)
+            for (int i = lane; i < m; i += 32) {
+              out.x[st + i] = src.x[st + i];
+              out.y[st + i] = src.y[st + i];
+              out.z[st + i] = src.z[st + i];
+              out.o[st + i] = src.o[st + i];
+            }
+          continue;
+        }
+        const T e0 = bx[3] - bx[0], e1 = bx[4] - bx[1], e2 = bx[5] - bx[2];
+        const int ax = e0 >= e1 ? (e0 >= e2 ? 0 : 2) : (e1 >= e2 ? 1 : 2);
+        const T ext = ax == 0 ? e0 : (ax == 1 ? e1 : e2);
+        const T lo = bx[ax];
+        const T inv = ext > (T)0 ? (T)kBins / ext : (T)0;
+        const int nl = left_size(m, bs);
+        const T* v = ax == 0 ? src.x : (ax == 1 ? src.y : src.z);
+#pragma unroll 8
+        for (int j = 0; j < 32; ++j) h[lane * 32 + j] = 0u;
+        __syncwarp();
+        for (int i = lane; i < m; i += 32) atomicAdd(&h[bin_of(v[st + i], lo, inv)], 1u);
+        __syncwarp();
+        int bstar, lt, midc;
+        find_split(h, nl, lane, bstar, lt, midc);
+        const int take = nl - lt;
+        int cl = 0, cm = 0, cr = 0;
+        T a[2][3], z[2][3];
+#pragma unroll
+        for (int k = 0; k < 2; ++k)
+#pragma unroll
+          for (int c = 0; c < 3; ++c) {
+            a[k][c] = pinf;
+            z[k][c] = -pinf;
+          }
+        for (int i0 = 0; i0 < m; i0 += 32) {
+          const int i = i0 + lane;
+          const bool live = i < m;
+          T p3[3] = {T(0), T(0), T(0)};
+          int32_t o = 0;
+          int cat = 3;
+          if (live) {
+            p3[0] = src.x[st + i];
+            p3[1] = src.y[st + i];
+            p3[2] = src.z[st + i];
+            o = src.o[st + i];
+            const int bn = bin_of(p3[ax], lo, inv);
+            cat = bn < bstar ? 0 : (bn == bstar ? 1 : 2);
+          }
+          const unsigned m0 = __ballot_sync(0xffffffffu, cat == 0);
+          const unsigned m1 = __ballot_sync(0xffffffffu, cat == 1);
+          const unsigned m2 = __ballot_sync(0xffffffffu, cat == 2);
+          const unsigned below = (1u << lane) - 1u;
+          int pos = 0;
+          if (cat == 0) {
+            pos = cl + __popc(m0 & below);
+          } else if (cat == 1) {
+            const int t = cm + __popc(m1 & below);
+            pos = t < take ? lt + t : nl + (t - take);
+          } else if (cat == 2) {
+            pos = nl + (midc - take) + cr + __popc(m2 & below);
+          }
+          cl += __popc(m0);
+          cm += __popc(m1);
+          cr += __popc(m2);
+          if (live) {
+            dst.x[st + pos] = p3[0];
+            dst.y[st + pos] = p3[1];
+            dst.z[st + pos] = p3[2];
+            dst.o[st + pos] = o;
+            const int k = pos < nl ? 0 : 1;
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+              a[k][c] = p3[c] < a[k][c] ? p3[c] : a[k][c];
+              z[k][c] = p3[c] > z[k][c] ? p3[c] : z[k][c];
+            }
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < 2; ++k)
+#pragma unroll
+          for (int c = 0; c < 3; ++c) {
+            a[k][c] = wmin(a[k][c]);
+            z[k][c] = wmax(z[k][c]);
+          }
+        // push right then left (left processed first; order is irrelevant)
+        if (top + 2 > kStack) __trap();  // depth <= log2(n / BS) + 1 < kStack
+        if (lane == 0) {
+          w_start[warp][top] = st + nl;
+          w_m[warp][top] = m - nl;
+          w_par[warp][top] = pr ^ 1;
+#pragma unroll
+          for (int c = 0; c < 3; ++c) {
+            w_box[warp][top][c] = a[1][c];
+            w_box[warp][top][3 + c] = z[1][c];
+          }
+          w_start[warp][top + 1] = st;
+          w_m[warp][top + 1] = nl;
+          w_par[warp][top + 1] = pr ^ 1;
+#pragma unroll
+          for (int c = 0; c < 3; ++c) {
+            w_box[warp][top + 1][c] = a[0][c];
+            w_box[warp][top + 1][3 + c] = z[0][c];
+          }
+        }
+        top += 2;
+        __syncwarp();
+      }
+    }
+  }
+  __syncthreads();
+
+  // 3. running distances, padding of the last bucket, bucket boxes
+  T* X = out.x;
+  T* Y = out.y;
+  T* Z = out.z;
+  int32_t* Ob = out.o;
+  for (int s = tid; s < n; s += kThreads) D[s] = pinf;
+  const int first_last = (int)((p.nbuckets - 1) * p.bs);
+  for (int s = n + tid; s < (int)p.nslots; s += kThreads) {
+    X[s] = X[first_last];
+    Y[s] = Y[first_last];
+    Z[s] = Z[first_last];
+    D[s] = -pinf;
+    Ob[s] = -1;
+  }
+  __syncthreads();
+  for (int q = warp; q < (int)p.nbuckets; q += kNW) {
+    T a[3] = {pinf, pinf, pinf}, z[3] = {-pinf, -pinf, -pinf};
+    for (int u = lane; u < bs; u += 32) {
+      const int s = q * bs + u;
+      const T v[3] = {X[s], Y[s], Z[s]};
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        a[c] = v[c] < a[c] ? v[c] : a[c];
+        z[c] = v[c] > z[c] ? v[c] : z[c];
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      a[c] = wmin(a[c]);
+      z[c] = wmax(z[c]);
+    }
+    if (lane == 0) {
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        BB[(int64_t)q * 6 + c] = a[c];
+        BB[(int64_t)q * 6 + 3 + c] = z[c];
+      }
+    }
+  }
+}
+
+// histograms + the per-warp stack boxes (sized for double)
+size_t bucket_kd_smem() {
+  return (size_t)kMaxSeg * kBins * sizeof(uint32_t) + (size_t)kNW * kStack * 6 * sizeof(double);
+}
+
+cudaError_t launch_bucket_kd(int dtype, const BucketBuildParams& p, int64_t batch,
+                             cudaStream_t st) {
+  const void* fn = dtype == 0 ? reinterpret_cast<const void*>(&bucket_kd_kernel<float>)
+                              : reinterpret_cast<const void*>(&bucket_kd_kernel<double>);
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)bucket_kd_smem());
+  if (e != cudaSuccess) return e;
+  void* args[] = {const_cast<BucketBuildParams*>(&p)};
+  return cudaLaunchKernel(fn, dim3((unsigned)batch), dim3(kThreads), args, bucket_kd_smem(), st);
+}
+
+}  // namespace ffps

@@ -107,12 +107,16 @@ struct GridInst {
   int nt;
   int ppl;
   int km;          // winners per round at most
-  const void* fn;  // fps_grid_kernel(BucketParams, int G)
+  int cl;          // CTAs per cloud (thread-block cluster size)
+  const void* fn;  // fps_grid_kernel(BucketParams)
   size_t esz;
 };
 const GridInst* grid_instances(int* count);
-size_t grid_smem(int dtype, int64_t nb, int G);
+size_t grid_smem(int dtype, int64_t nb);
 size_t bucket_build_smem();
+size_t bucket_kd_smem();
+cudaError_t launch_bucket_kd(int dtype, const BucketBuildParams& p, int64_t batch,
+                             cudaStream_t st);
 cudaError_t launch_bucket_build(int dtype, const BucketBuildParams& p, int64_t batch,
                                 cudaStream_t st);
 

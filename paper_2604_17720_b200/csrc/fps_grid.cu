@@ -42,8 +42,11 @@ namespace ffps {
 
 namespace {
 
-constexpr int kMaxCells = 27;  // a bucket registered in at most this many cells
-constexpr int kEntryBudget = 12;  // cell entries per bucket on average (shared budget)
+constexpr int kGS = 32;  // buckets per group of the two-level index (one per lane)
+constexpr int kTraceW = 16;  // trace words per round and warp (FFPS_TRACE_GRID)
+// rounds re-test every bucket while the search radius is this large a fraction
+// of the cloud's extent (little to prune, the whole CTA shares the work)
+constexpr double kFullFrac = 0.375;
 
 template <typename A>
 __device__ __forceinline__ int argmax_lane_g(typename A::bits_t v, uint32_t i) {
@@ -68,72 +71,140 @@ __device__ __forceinline__ double box_lb(double px, double py, double pz, const 
 
 }  // namespace
 
-// dynamic shared memory bytes of fps_grid_kernel for nb buckets
+// dynamic shared memory bytes of fps_grid_kernel for nb buckets (per CTA)
 template <typename T>
-__host__ __device__ constexpr size_t grid_smem_bytes(int64_t nb, int G) {
+__host__ __device__ constexpr size_t grid_smem_bytes(int64_t nb) {
   return (size_t)nb * (6 * sizeof(T) + 3 * sizeof(T) + 2 * sizeof(typename Arith<T>::bits_t) +
-                       4 /*ki*/ + 4 /*pmask*/ + 4 /*rlist*/ + 2 /*olist*/ +
-                       2 * kEntryBudget /*cell entries*/) +
-         ((size_t)G * G * G + 1) * 4;
+                       4 /*ki*/ + 4 /*pmask*/ + 4 /*rlist*/) +
+         (size_t)((nb + kGS - 1) / kGS) *
+             (6 * sizeof(T) + 3 * sizeof(typename Arith<T>::bits_t) + 4 * 4);
 }
 
-template <typename T, int NT, int PPL, int KM>
-__global__ void __launch_bounds__(NT, 1) fps_grid_kernel(const BucketParams prm, int G) {
+
+
+// DSMEM record of a cluster rank's local top list (CL > 1), 32-bit words:
+// float  [v, pos, x, y, z, v2, q, flag]                     (8 words)
+// double [v lo, v hi, v2 lo, v2 hi, x, x, y, y, z, z, pos, q, flag, pad x3] (16)
+template <typename T>
+struct GridRec;
+template <>
+struct GridRec<float> {
+  static constexpr int W = 8;
+
+  __device__ static void send(uint32_t dst, uint32_t bar, int32_t v, int32_t v2, uint32_t pos,
+                              int q, float x, float y, float z, uint32_t flag) {
+    st_async_v4(dst, bar, (uint32_t)v, pos, __float_as_uint(x), __float_as_uint(y));
+    st_async_v4(dst + 16, bar, __float_as_uint(z), (uint32_t)v2, (uint32_t)q, flag);
+  }
+  __device__ static int32_t v(const uint32_t* w) { return (int32_t)w[0]; }
+  __device__ static int32_t v2(const uint32_t* w) { return (int32_t)w[5]; }
+  __device__ static uint32_t pos(const uint32_t* w) { return w[1]; }
+  __device__ static int q(const uint32_t* w) { return (int)w[6]; }
+  __device__ static uint32_t flag(const uint32_t* w) { return w[7]; }
+  __device__ static float c(const uint32_t* w, int i) { return __uint_as_float(w[2 + i]); }
+};
+template <>
+struct GridRec<double> {
+  static constexpr int W = 16;
+
+  __device__ static void send(uint32_t dst, uint32_t bar, int64_t v, int64_t v2, uint32_t pos,
+                              int q, double x, double y, double z, uint32_t flag) {
+    st_async_v2_b64(dst, bar, (uint64_t)v, (uint64_t)v2);
+    st_async_v2_b64(dst + 16, bar, (uint64_t)__double_as_longlong(x),
+                    (uint64_t)__double_as_longlong(y));
+    st_async_v2_b64(dst + 32, bar, (uint64_t)__double_as_longlong(z),
+                    (uint64_t)pos | ((uint64_t)(uint32_t)q << 32));
+    st_async_v2_b64(dst + 48, bar, (uint64_t)flag, 0ull);
+  }
+  __device__ static int64_t u64(const uint32_t* w, int i) {
+    return (int64_t)(((uint64_t)w[2 * i + 1] << 32) | w[2 * i]);
+  }
+  __device__ static int64_t v(const uint32_t* w) { return u64(w, 0); }
+  __device__ static int64_t v2(const uint32_t* w) { return u64(w, 1); }
+  __device__ static uint32_t pos(const uint32_t* w) { return w[10]; }
+  __device__ static int q(const uint32_t* w) { return (int)w[11]; }
+  __device__ static uint32_t flag(const uint32_t* w) { return w[12]; }
+  __device__ static double c(const uint32_t* w, int i) { return __longlong_as_double(u64(w, 2 + i)); }
+};
+
+// CL = CTAs per cloud (thread-block cluster): bucket q belongs to rank q % CL
+// and is row q / CL of that rank's table.  Each rank flags, re-evaluates and
+// ranks its own buckets; the ranks' top-KM lists are exchanged through DSMEM
+// (st.async + mbarrier, double-buffered by round parity) and merged
+// identically by every warp of every rank.
+template <typename T, int NT, int PPL, int KM, int CL>
+__global__ void __launch_bounds__(NT, 1) fps_grid_kernel(const BucketParams prm) {
   using A = Arith<T>;
   using bits_t = typename A::bits_t;
   constexpr int NW = NT / 32;
   constexpr int BS = 32 * PPL;
   constexpr uint32_t kNoIdx = 0xffffffffu;
-  constexpr int NREC = 128;
-  constexpr int RPL = NREC / 32;
   static_assert(KM <= 32, "one candidate per lane in the chain test");
   static_assert(NW >= KM, "KM warp maxima, at least one warp per point");
-  constexpr int WPP = NW / KM >= 2 ? 2 : 1;  // warps per selected point in the flag phase
 
-  const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int nb = (int)prm.nbuckets;
-  const int NC = G * G * G;
+  static_assert(CL == 1 || CL == 2 || CL == 4, "cluster of 1, 2 or 4 CTAs");
+  static_assert(CL * KM <= 32, "one exchanged record per lane");
+  using R = GridRec<T>;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int rank = CL > 1 ? (int)cluster_ctarank() : 0;
+  const int b = (int)blockIdx.x / CL;  // cloud
+  const int nb = ((int)prm.nbuckets - rank + CL - 1) / CL;  // buckets of this rank
+  const int ng = (nb + kGS - 1) / kGS;  // bucket groups (kGS consecutive table rows)
   const int64_t off = (int64_t)b * prm.nslots;
   const T* __restrict__ X = static_cast<const T*>(prm.X) + off;
   const T* __restrict__ Y = static_cast<const T*>(prm.Y) + off;
   const T* __restrict__ Z = static_cast<const T*>(prm.Z) + off;
   T* __restrict__ D = static_cast<T*>(prm.D) + off;
   const int32_t* __restrict__ O = prm.O + off;
-  const T* __restrict__ BB = static_cast<const T*>(prm.BB) + (int64_t)b * nb * 6;
+  const T* __restrict__ BB = static_cast<const T*>(prm.BB) + (int64_t)b * prm.nbuckets * 6;
 
   // ---- shared memory -----------------------------------------------------------
   extern __shared__ __align__(16) unsigned char smem[];
   T* box = reinterpret_cast<T*>(smem);                   // [nb][6]
-  T* kx = box + (size_t)nb * 6;                          // [nb][3] key point xyz
+  // groups: union box and max key of kGS consecutive rows (kd / Morton order
+  // keeps them spatially compact); max keys refreshed every round (phase C)
+  T* gbox = box + (size_t)nb * 6;                        // [ng][6]
+  T* kx = gbox + (size_t)ng * 6;                         // [nb][3] key point xyz
   bits_t* kv = reinterpret_cast<bits_t*>(kx + (size_t)nb * 3);  // [nb] key value
   bits_t* k2 = kv + nb;                                  // [nb] second-best value
-  uint32_t* ki = reinterpret_cast<uint32_t*>(k2 + nb);   // [nb] key position
+  // per group (phase C): best and second-best key (value, position, row), third value
+  bits_t* gmax = k2 + nb;                                // [ng] group max key
+  bits_t* g2v = gmax + ng;                               // [ng]
+  bits_t* g3v = g2v + ng;                                // [ng]
+  uint32_t* ki = reinterpret_cast<uint32_t*>(g3v + ng);  // [nb] key position
   uint32_t* pmask = ki + nb;                             // [nb] flagging points of the round
   int32_t* rlist = reinterpret_cast<int32_t*>(pmask + nb);  // [nb] round list
-  uint32_t* coff = reinterpret_cast<uint32_t*>(rlist + nb);  // [NC + 1] cell -> end offset
-  uint16_t* cent = reinterpret_cast<uint16_t*>(coff + NC + 1);  // [nb * kEntryBudget]
-  uint16_t* olist = cent + (size_t)nb * kEntryBudget;           // [nb] oversize buckets
-  __shared__ bits_t wm_s[NW];
-  __shared__ bits_t rv_s[NREC], r2_s[NREC];
-  __shared__ uint32_t ri_s[NREC];
-  __shared__ int32_t rq_s[NREC];
-  __shared__ T rx_s[NREC][3];
+  uint32_t* gp1 = reinterpret_cast<uint32_t*>(rlist + nb);  // [ng]
+  uint32_t* gp2 = gp1 + ng;                                 // [ng]
+  int32_t* gq1 = reinterpret_cast<int32_t*>(gp2 + ng);     // [ng] table row of the best
+  int32_t* gq2 = gq1 + ng;                                  // [ng]
+  constexpr int CPL = 8;  // candidates per lane in phase R (2 * ng <= 256)
+  // phase D: per-warp candidate list (<= 32)
+  __shared__ bits_t cv_w[1][32];
+  __shared__ uint32_t ci_w[1][32];
+  __shared__ int16_t cq_w[1][32];
+  __shared__ int16_t top_s[KM];  // phase R: rows of the ranked top-KM candidates
+  __shared__ bits_t topv_s[KM];
   // accepted points of the last round: every warp keeps its own copy (all
   // warps derive the same set from the candidate list, no barrier needed)
-  __shared__ T sp_w[NW][KM][3];
-  __shared__ uint32_t si_w[NW][KM];
-  __shared__ int32_t sq_w[NW][KM];
-  __shared__ int16_t top_w[NW][KM];
-  __shared__ int ncand_s, rcount_s, ocount_s, ebudget_s;
-  __shared__ T glo_s[3], ginv_s[3];
+  __shared__ T sp_w[1][KM][3];
+  __shared__ uint32_t si_w[1][KM];
+  __shared__ int32_t sq_w[1][KM];
+  __shared__ int16_t top_w[1][KM];
+  __shared__ int acc_s;
+  __shared__ bits_t rmax_s;
+  __shared__ int rcount_s;
+  __shared__ T ext_s;
   __shared__ T red_s[2][NW][3];
-  __shared__ uint32_t cscr_s[NW][2][32];  // per-warp cell scratch of the flag phase
+  // CL > 1: incoming top lists [parity][rank * KM + e], one mbarrier per parity
+  __shared__ __align__(16) uint32_t xrec_s[CL > 1 ? 2 : 1][CL > 1 ? CL * KM * R::W : 1];
+  __shared__ __align__(8) uint64_t xbar_s[2];
 
   // ---- bucket table ------------------------------------------------------------
   T lo[3] = {A::pinf(), A::pinf(), A::pinf()}, hi[3] = {A::ninf(), A::ninf(), A::ninf()};
   for (int q = tid; q < nb; q += NT) {
 #pragma unroll
-    for (int c = 0; c < 6; ++c) box[q * 6 + c] = BB[(int64_t)q * 6 + c];
+    for (int c = 0; c < 6; ++c) box[q * 6 + c] = BB[((int64_t)q * CL + rank) * 6 + c];
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
       lo[c] = box[q * 6 + c] < lo[c] ? box[q * 6 + c] : lo[c];
@@ -144,8 +215,7 @@ __global__ void __launch_bounds__(NT, 1) fps_grid_kernel(const BucketParams prm,
     kx[q * 3 + 0] = kx[q * 3 + 1] = kx[q * 3 + 2] = T(0);
     pmask[q] = 0u;
   }
-  for (int c = tid; c <= NC; c += NT) coff[c] = 0u;
-  // cloud box -> grid
+  // cloud extent (rounds with a search radius close to it test every bucket)
 #pragma unroll
   for (int c = 0; c < 3; ++c) {
     for (int o = 16; o > 0; o >>= 1) {
@@ -158,104 +228,71 @@ __global__ void __launch_bounds__(NT, 1) fps_grid_kernel(const BucketParams prm,
       red_s[1][warp][c] = hi[c];
     }
   }
+  if (tid == 0) rcount_s = 0;
+  __syncthreads();
   if (tid == 0) {
-    ocount_s = 0;
-    rcount_s = 0;
-    ebudget_s = nb * kEntryBudget;
-  }
-  __syncthreads();
-  if (tid < 3) {
-    T a = A::pinf(), z = A::ninf();
-    for (int w = 0; w < NW; ++w) {
-      a = red_s[0][w][tid] < a ? red_s[0][w][tid] : a;
-      z = red_s[1][w][tid] > z ? red_s[1][w][tid] : z;
+    T e = T(0);
+    for (int c = 0; c < 3; ++c) {
+      T a = A::pinf(), z = A::ninf();
+      for (int w = 0; w < NW; ++w) {
+        a = red_s[0][w][c] < a ? red_s[0][w][c] : a;
+        z = red_s[1][w][c] > z ? red_s[1][w][c] : z;
+      }
+      e = z - a > e ? z - a : e;
     }
-    glo_s[tid] = a;
-    ginv_s[tid] = z > a ? (T)G / (z - a) : T(0);
+    ext_s = e;
   }
-  __syncthreads();
-  const T glo[3] = {glo_s[0], glo_s[1], glo_s[2]}, ginv[3] = {ginv_s[0], ginv_s[1], ginv_s[2]};
-  auto cellc = [&](T v, int c) -> int {  // monotone in v
-    const int i = (int)((v - glo[c]) * ginv[c]);
-    return i < 0 ? 0 : (i >= G ? G - 1 : i);
-  };
-  // register every bucket in the cells its box overlaps (<= kMaxCells cells,
-  // within the shared entry budget), the rest as oversize; pmask marks the
-  // registered buckets during the build
-  for (int pass = 0; pass < 2; ++pass) {
-    for (int q = tid; q < nb; q += NT) {
-      int c0[3], c1[3];
+  // group boxes
+  for (int g = tid; g < ng; g += NT) {
+    T a[3] = {A::pinf(), A::pinf(), A::pinf()}, z[3] = {A::ninf(), A::ninf(), A::ninf()};
+    const int q1 = (g + 1) * kGS < nb ? (g + 1) * kGS : nb;
+    for (int q = g * kGS; q < q1; ++q)
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
-        c0[c] = cellc(box[q * 6 + c], c);
-        c1[c] = cellc(box[q * 6 + 3 + c], c);
+        a[c] = box[q * 6 + c] < a[c] ? box[q * 6 + c] : a[c];
+        z[c] = box[q * 6 + 3 + c] > z[c] ? box[q * 6 + 3 + c] : z[c];
       }
-      const int cnt = (c1[0] - c0[0] + 1) * (c1[1] - c0[1] + 1) * (c1[2] - c0[2] + 1);
-      if (pass == 0) {
-        const bool reg = cnt <= kMaxCells && atomicSub(&ebudget_s, cnt) >= cnt;
-        pmask[q] = reg ? 1u : 0u;
-        if (!reg) {
-          olist[atomicAdd(&ocount_s, 1)] = (uint16_t)q;
-          continue;
-        }
-      } else if (pmask[q] == 0u) {
-        continue;
-      }
-      for (int x = c0[0]; x <= c1[0]; ++x)
-        for (int y = c0[1]; y <= c1[1]; ++y)
-          for (int z = c0[2]; z <= c1[2]; ++z) {
-            const int cell = (x * G + y) * G + z;
-            if (pass == 0) atomicAdd(&coff[cell + 1], 1u);
-            else cent[atomicAdd(&coff[cell], 1u)] = (uint16_t)q;
-          }
-    }
-    __syncthreads();
-    if (pass == 0) {  // exclusive scan: coff[c] = start of cell c
-      if (warp == 0) {
-        uint32_t carry = 0;
-        for (int c0 = 0; c0 <= NC; c0 += 32) {
-          const int c = c0 + lane;
-          uint32_t v = c <= NC ? coff[c] : 0u;
 #pragma unroll
-          for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t u = __shfl_up_sync(0xffffffffu, v, o);
-            if (lane >= o) v += u;
-          }
-          if (c <= NC) coff[c] = v + carry;
-          carry += __shfl_sync(0xffffffffu, v, 31);
-        }
-      }
-      __syncthreads();
+    for (int c = 0; c < 3; ++c) {
+      gbox[g * 6 + c] = a[c];
+      gbox[g * 6 + 3 + c] = z[c];
     }
+    gmax[g] = A::bits(A::pinf());
   }
-  for (int q = tid; q < nb; q += NT) pmask[q] = 0u;
   __syncthreads();
-  // after the fill pass coff[c] = end of cell c (= start of c + 1), start(c) = coff[c - 1]
+  const T full_r = (T)(kFullFrac * (double)ext_s);
 
   // ---- seed (fps_core.py:124-130) -----------------------------------------------
   const int seed = (int)prm.seed_pos[b];
   int64_t* order = prm.order + (int64_t)b * prm.out_stride;
   T* sel = static_cast<T*>(prm.sel_d2) + (int64_t)b * prm.out_stride;
-  if (lane == 0) {
+  if (tid == 0) {
     const T* X0 = static_cast<const T*>(prm.xyz) + (int64_t)b * prm.cloud_stride * 3;
     const int64_t src = prm.index_map ? prm.index_map[(int64_t)b * prm.map_stride + seed] : seed;
-    sp_w[warp][0][0] = X0[3 * src + 0];
-    sp_w[warp][0][1] = X0[3 * src + 1];
-    sp_w[warp][0][2] = X0[3 * src + 2];
-    si_w[warp][0] = (uint32_t)seed;
-    sq_w[warp][0] = -1;
+    sp_w[0][0][0] = X0[3 * src + 0];
+    sp_w[0][0][1] = X0[3 * src + 1];
+    sp_w[0][0][2] = X0[3 * src + 2];
+    si_w[0][0] = (uint32_t)seed;
+    sq_w[0][0] = -1;
   }
-  if (tid == 0) {
+  if (tid == 0 && rank == 0) {
     order[0] = seed;
     sel[0] = A::pinf();
+  }
+  if constexpr (CL > 1) {
+    if (tid == 0) {
+      mbar_init(smem_u32(&xbar_s[0]), 1);
+      mbar_init(smem_u32(&xbar_s[1]), 1);
+      fence_mbar_init_cluster();
+    }
+    cluster_sync_all();  // peers' mbarriers initialised before any push
   }
   int J = 1;                        // points accepted by the last round
   bits_t rmax = A::bits(A::pinf());  // upper bound of every key (R^2 of the cube)
   __syncthreads();
   const int iters = (int)prm.iters;
-  const int nover = ocount_s;
   long long* trace =
-      (prm.trace && b == 0 && lane == 0) ? prm.trace + (int64_t)warp * prm.trace_iters * 8 : nullptr;
+      (prm.trace && b == 0 && rank == 0 && lane == 0) ? prm.trace + (int64_t)warp * prm.trace_iters * kTraceW : nullptr;
 
   auto flag = [&](int q, int t) {  // OR point t into bucket q's mask, list it once
     const uint32_t old = atomicOr(&pmask[q], 1u << t);
@@ -282,86 +319,50 @@ __global__ void __launch_bounds__(NT, 1) fps_grid_kernel(const BucketParams prm,
   int k = 1;
   for (int round = 0; k < iters; ++round) {
     long long t0 = 0, t1 = 0, t2 = 0, t3 = 0;
-    int ntest_w = 0;  // traced: entries tested by this warp
+    long long td[7] = {0, 0, 0, 0, 0, 0, 0};  // warp 0: sub-steps of phase D
+    int ntest_w = 0;  // traced: hit groups of this warp
+    int ncand_w = 0;  // traced: candidates of this warp
     if (trace) t0 = clock64();
+    if constexpr (CL > 1)
+      if (tid == 0)
+        mbar_arrive_expect_tx(smem_u32(&xbar_s[round & 1]), CL * KM * R::W * 4);
     // A. flag ---------------------------------------------------------------------
     const T r2 = A::from_bits(rmax);
-    // half-width of the search cube, padded for the rounding of p +- R
-    const T R = round == 0 ? A::pinf() : (T)(sqrt((double)r2) * 1.001) ;
-    bool full = round == 0 || !(R * ginv[0] < T(3)) || !(R * ginv[1] < T(3)) ||
-                !(R * ginv[2] < T(3));
+    // search radius: every key is <= R^2 (padded for the rounding of sqrt)
+    const T R = round == 0 ? A::pinf() : (T)(sqrt((double)r2) * 1.001);
+    const bool full = round == 0 || !(R < full_r);
     if (full) {  // every bucket against every point
       for (int q = tid; q < nb; q += NT) {
         if (round == 0) {
           flag(q, 0);
           continue;
         }
-        for (int t = 0; t < J; ++t) test(q, t, sp_w[warp][t][0], sp_w[warp][t][1], sp_w[warp][t][2]);
+        for (int t = 0; t < J; ++t) test(q, t, sp_w[0][t][0], sp_w[0][t][1], sp_w[0][t][2]);
       }
-      if (round > 0 && warp == 0 && lane < J && sq_w[0][lane] >= 0)
-        flag(sq_w[0][lane], lane);  // the point -> -inf
+      if (round > 0 && warp == 0 && lane < J && sq_w[0][lane] >= 0 &&
+          sq_w[0][lane] % CL == rank)
+        flag(sq_w[0][lane] / CL, lane);  // the point -> -inf
     } else {
-      // two warps per point (NW >= 2 * KM); the (cell, entry) pairs of the
-      // point's cube are spread over the 64 lanes: per chunk of 32 cells the
-      // warp publishes each cell's first entry and inclusive entry count in
-      // shared scratch, then every lane walks flat entry indices
-      for (int t = warp / WPP; t < J; t += NW / WPP) {
-        const int half = warp % WPP;
-        const T px = sp_w[warp][t][0], py = sp_w[warp][t][1], pz = sp_w[warp][t][2];
-        const T pad = (fabs(px) + fabs(py) + fabs(pz) + T(1)) * T(1e-6);
-        int c0[3], c1[3];
-        const T pc[3] = {px, py, pz};
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-          c0[c] = cellc(pc[c] - R - pad, c);
-          c1[c] = cellc(pc[c] + R + pad, c);
-        }
-        const int ny = c1[1] - c0[1] + 1, nz = c1[2] - c0[2] + 1;
-        const int ncells = (c1[0] - c0[0] + 1) * ny * nz;
-        uint32_t* cs = cscr_s[warp][0];  // first entry of each cell of the chunk
-        uint32_t* ci = cscr_s[warp][1];  // inclusive entry count
-        for (int cb = 0; cb < ncells; cb += 32) {
-          const int i = cb + lane;
-          uint32_t e0 = 0, cntc = 0;
-          if (i < ncells) {
-            const int x = c0[0] + i / (ny * nz), y = c0[1] + (i / nz) % ny, z = c0[2] + i % nz;
-            const int cell = (x * G + y) * G + z;
-            e0 = cell == 0 ? 0u : coff[cell - 1];
-            cntc = coff[cell] - e0;
+      // wpp warps per selected point: test the group boxes against the group
+      // max keys (a group with box_d2 >= its max key holds no bucket the point
+      // can flag), then the kGS buckets of every hit group (one per lane)
+      const int wpp = NW / J;
+      if (warp < J * wpp) {
+        const int t = warp / wpp, sub = warp % wpp;
+        const T px = sp_w[0][t][0], py = sp_w[0][t][1], pz = sp_w[0][t][2];
+        for (int g0 = sub * 32; g0 < ng; g0 += wpp * 32) {
+          const int g = g0 + lane;
+          const bool hit = g < ng && !(box_lb(px, py, pz, gbox + (size_t)g * 6) >= A::from_bits(gmax[g]));
+          unsigned m = __ballot_sync(0xffffffffu, hit);
+          ntest_w += __popc(m);
+          while (m) {
+            const int q = (g0 + __ffs(m) - 1) * kGS + lane;
+            m &= m - 1u;
+            test_warp(q < nb, q < nb ? q : 0, t, px, py, pz);
           }
-          uint32_t incl = cntc;
-#pragma unroll
-          for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t u = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += u;
-          }
-          const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
-          ntest_w += (int)total;
-          cs[lane] = e0;
-          ci[lane] = incl;
-          __syncwarp();
-          for (uint32_t f0 = 32 * half; f0 < total; f0 += 32 * WPP) {  // uniform trip count
-            const uint32_t f = f0 + lane;
-            int q = 0;
-            if (f < total) {
-              int lo_l = 0, hi_l = 31;  // lowest cell whose inclusive count > f
-              while (lo_l < hi_l) {
-                const int mid = (lo_l + hi_l) >> 1;
-                if (ci[mid] > f) hi_l = mid;
-                else lo_l = mid + 1;
-              }
-              const uint32_t before = lo_l == 0 ? 0u : ci[lo_l - 1];
-              q = cent[cs[lo_l] + (f - before)];
-            }
-            test_warp(f < total, q, t, px, py, pz);
-          }
-          __syncwarp();
         }
-        for (int i0 = 32 * half; i0 < nover; i0 += 32 * WPP) {
-          const int i = i0 + lane;
-          test_warp(i < nover, i < nover ? olist[i] : 0, t, px, py, pz);
-        }
-        if (lane == 0 && half == 0 && sq_w[warp][t] >= 0) flag(sq_w[warp][t], t);  // -> -inf
+        if (lane == 0 && sub == 0 && sq_w[0][t] >= 0 && sq_w[0][t] % CL == rank)
+          flag(sq_w[0][t] / CL, t);  // the point -> -inf
       }
     }
     if (trace) t1 = clock64();
@@ -380,7 +381,7 @@ __global__ void __launch_bounds__(NT, 1) fps_grid_kernel(const BucketParams prm,
         pm[c] = pmask[qc[c]];
 #pragma unroll
         for (int u = 0; u < PPL; ++u) {
-          const int64_t s = (int64_t)qc[c] * BS + u * 32 + lane;
+          const int64_t s = ((int64_t)qc[c] * CL + rank) * BS + u * 32 + lane;
           xs[c][u] = X[s];
           ys[c][u] = Y[s];
           zs[c][u] = Z[s];
@@ -395,8 +396,8 @@ __global__ void __launch_bounds__(NT, 1) fps_grid_kernel(const BucketParams prm,
         while (m) {  // only the points that flagged the bucket can change it
           const int t = __ffs(m) - 1;
           m &= m - 1u;
-          const T px = sp_w[warp][t][0], py = sp_w[warp][t][1], pz = sp_w[warp][t][2];
-          const uint32_t pw = si_w[warp][t];
+          const T px = sp_w[0][t][0], py = sp_w[0][t][1], pz = sp_w[0][t][2];
+          const uint32_t pw = si_w[0][t];
 #pragma unroll
           for (int u = 0; u < PPL; ++u) {
             T nd = A::vmin(ds[c][u], A::d2(xs[c][u], ys[c][u], zs[c][u], px, py, pz));  // :93
@@ -413,7 +414,8 @@ __global__ void __launch_bounds__(NT, 1) fps_grid_kernel(const BucketParams prm,
         T x1 = T(0), y1 = T(0), z1 = T(0);
 #pragma unroll
         for (int u = 0; u < PPL; ++u) {
-          if (A::bits(ds[c][u]) != A::bits(d0[c][u])) D[(int64_t)q * BS + u * 32 + lane] = ds[c][u];
+          if (A::bits(ds[c][u]) != A::bits(d0[c][u]))
+            D[((int64_t)q * CL + rank) * BS + u * 32 + lane] = ds[c][u];
           const bits_t v = A::bits(ds[c][u]);
           if (v > b1 || (v == b1 && os[c][u] < i1)) {
             b2 = b1;
@@ -448,173 +450,302 @@ __global__ void __launch_bounds__(NT, 1) fps_grid_kernel(const BucketParams prm,
     if (trace) t2 = clock64();
     __syncthreads();  // keys final for this round
     if (tid == 0) rcount_s = 0;
-    // C. candidates: keys >= tau, tau = smallest warp maximum over table slices ------
-    const int per = (nb + NW - 1) / NW;
-    const int s0 = warp * per, s1 = s0 + per < nb ? s0 + per : nb;
+    // C. group statistics (each warp refreshes a slice of whole groups, one
+    //    bucket per lane): top-2 keys by (value desc, position asc) + third value
     {
-      bits_t mv = A::kmin;
-      for (int q = s0 + lane; q < s1; q += 32) mv = kv[q] > mv ? kv[q] : mv;
-      mv = A::warp_max(mv);
-      if (lane == 0) wm_s[warp] = mv;
-      if (tid == 0) ncand_s = 0;
-    }
-    __syncthreads();
-    {
-      // tau = the KM-th largest warp maximum: KM warps hold a key >= tau, so
-      // the global top-KM is among the keys >= tau (ties at tau included)
-      bits_t tau;
-      {
-        const bits_t mine = lane < NW ? wm_s[lane] : A::kmin;
-        int rank = 0;
-#pragma unroll
-        for (int w = 0; w < NW; ++w) {
-          const bits_t o = wm_s[w];
-          rank += (o > mine || (o == mine && w < lane)) ? 1 : 0;
-        }
-        const unsigned hit = __ballot_sync(0xffffffffu, lane < NW && rank == KM - 1);
-        tau = A::shfl(mine, hit ? __ffs(hit) - 1 : 0);
-      }
-      for (int q0 = s0; q0 < s1; q0 += 32) {
-        const int q = q0 + lane;
-        const bool c = q < s1 && kv[q] >= tau && kv[q] != A::kmin;
-        const unsigned m = __ballot_sync(0xffffffffu, c);
-        if (m) {
-          int base = 0;
-          if (lane == 0) base = atomicAdd(&ncand_s, __popc(m));
-          base = __shfl_sync(0xffffffffu, base, 0);
-          const int e = base + __popc(m & ((1u << lane) - 1u));
-          if (c && e < NREC) {
-            rv_s[e] = kv[q];
-            ri_s[e] = ki[q];
-            r2_s[e] = k2[q];
-            rq_s[e] = q;
-            rx_s[e][0] = kx[q * 3 + 0];
-            rx_s[e][1] = kx[q * 3 + 1];
-            rx_s[e][2] = kx[q * 3 + 2];
-          }
+      const int gpw = (ng + NW - 1) / NW;
+      const int g_lo = warp * gpw, g_hi = g_lo + gpw < ng ? g_lo + gpw : ng;
+      for (int g = g_lo; g < g_hi; ++g) {
+        const int q = g * kGS + lane;
+        const bool in = q < nb;
+        bits_t v = in ? kv[q] : A::kmin;
+        const uint32_t p = in ? ki[q] : kNoIdx;
+        const bits_t m1 = A::warp_max(v);
+        const uint32_t p1 = __reduce_min_sync(0xffffffffu, v == m1 ? p : kNoIdx);
+        const unsigned w1 = __ballot_sync(0xffffffffu, v == m1 && p == p1);
+        if (w1 & (1u << lane)) v = A::kmin;
+        const bits_t m2 = A::warp_max(v);
+        const uint32_t p2 = __reduce_min_sync(0xffffffffu, v == m2 ? p : kNoIdx);
+        const unsigned w2 = __ballot_sync(0xffffffffu, v == m2 && p == p2) & ~w1;
+        if (w2 & (1u << lane)) v = A::kmin;
+        const bits_t m3 = A::warp_max(v);
+        if (lane == 0) {
+          gmax[g] = m1;
+          gp1[g] = p1;
+          gq1[g] = w1 ? g * kGS + __ffs(w1) - 1 : 0;
+          g2v[g] = m2;
+          gp2[g] = p2;
+          gq2[g] = w2 ? g * kGS + __ffs(w2) - 1 : 0;
+          g3v[g] = m3;
         }
       }
     }
     if (trace) t3 = clock64();
-    __syncthreads();  // candidate list complete
-    // D. every warp: top-KM of the list by rank, chain test, accepted prefix --------
-    //    (identical in all warps; warp 0 reports them)
-    const int ncand = ncand_s;
-    int acc = 1;
-    if (ncand > NREC) {
-      // massive ties: one exact winner from the whole table this round
-      bits_t bv = A::kmin;
-      uint32_t bi = kNoIdx;
-      int bq = 0;
-      for (int q = lane; q < nb; q += 32)
-        if (kv[q] > bv || (kv[q] == bv && ki[q] < bi)) {
-          bv = kv[q];
-          bi = ki[q];
-          bq = q;
+    __syncthreads();  // group statistics final
+    // R. all warps: rank the candidates = the top-2 keys of every group
+    //    (candidate c: group c >> 1, slot c & 1).  Lane j of every warp holds
+    //    candidates j, j + 32, ...; warp w ranks c = w, w + NW, ... with one
+    //    ballot per lane slot; ranks < KM go to top_s (rows) / topv_s.
+    const int ncd = 2 * ng;
+    const int nj = (ncd + 31) / 32;
+    bits_t cvv[CPL];
+    uint32_t cpp[CPL];
+#pragma unroll
+    for (int j = 0; j < CPL; ++j) {
+      const int c = j * 32 + lane;
+      const bool in = j < nj && c < ncd;
+      cvv[j] = in ? ((c & 1) ? g2v[c >> 1] : gmax[c >> 1]) : A::kmin;
+      cpp[j] = in ? ((c & 1) ? gp2[c >> 1] : gp1[c >> 1]) : kNoIdx;
+    }
+    for (int c = warp; c < ncd; c += NW) {
+      const bits_t vc = (c & 1) ? g2v[c >> 1] : gmax[c >> 1];
+      if (vc == A::kmin) continue;
+      const uint32_t pc = (c & 1) ? gp2[c >> 1] : gp1[c >> 1];
+      int rk = 0;
+#pragma unroll
+      for (int j = 0; j < CPL; ++j) {
+        if (j >= nj) break;
+        rk += __popc(__ballot_sync(0xffffffffu, cvv[j] > vc || (cvv[j] == vc && cpp[j] < pc)));
+      }
+      if (lane == 0 && rk < KM) {
+        top_s[rk] = (int16_t)((c & 1) ? gq2[c >> 1] : gq1[c >> 1]);
+        topv_s[rk] = vc;
+      }
+    }
+    __syncthreads();  // candidate ranks final
+    // D. warp 0 alone: this rank's top-KM keys (table rows, rank order).
+    //    tau2 = the KM-th candidate: a group whose third key reaches it may
+    //    hold a top-KM key that is not a candidate -> the general path: every
+    //    key >= tau2 of the groups with max >= tau2 (KM keys are >= tau2),
+    //    more than 32 of them (massive ties) -> the exact maximum alone, marked
+    //    truncated.
+    if (warp == 0) {
+    int nl = 0;
+    bool trunc = false;
+    {
+      const unsigned below = (1u << lane) - 1u;
+      int nvalid = 0;
+#pragma unroll
+      for (int j = 0; j < CPL; ++j) nvalid += __popc(__ballot_sync(0xffffffffu, cvv[j] != A::kmin));
+      const bits_t tau2 = nvalid >= KM ? topv_s[KM - 1] : A::kmin;
+      bool general = false;
+      for (int g0 = 0; g0 < ng; g0 += 32) {
+        const bits_t t3 = g0 + lane < ng ? g3v[g0 + lane] : A::kmin;
+        general |= __any_sync(0xffffffffu, t3 != A::kmin && t3 >= tau2);
+      }
+      if (trace) td[0] = clock64();
+      int nct = nvalid;
+      if (!general) {
+        nl = nvalid < KM ? nvalid : KM;
+        if (lane < nl) top_w[0][lane] = top_s[lane];
+      } else {
+        nct = 0;
+#pragma unroll 1
+        for (int j = 0; j < (ng + 31) / 32; ++j) {
+          const int gj = j * 32 + lane;
+          const bits_t gvj = gj < ng ? gmax[gj] : A::kmin;
+          unsigned hm = __ballot_sync(0xffffffffu, gvj >= tau2 && gvj != A::kmin);
+          while (hm) {
+            const int q = (j * 32 + __ffs(hm) - 1) * kGS + lane;
+            hm &= hm - 1u;
+            const bits_t v = q < nb ? kv[q] : A::kmin;
+            const bool c = v >= tau2 && v != A::kmin;
+            const unsigned cm = __ballot_sync(0xffffffffu, c);
+            const int slot = nct + __popc(cm & below);
+            if (c && slot < 32) {
+              cv_w[0][slot] = v;
+              ci_w[0][slot] = ki[q];
+              cq_w[0][slot] = (int16_t)q;
+            }
+            nct += __popc(cm);
+          }
         }
-      const int wl = argmax_lane_g<A>(bv, bi);
-      const int q = __shfl_sync(0xffffffffu, bq, wl);
-      if (lane == 0) {
-        sp_w[warp][0][0] = kx[q * 3 + 0];
-        sp_w[warp][0][1] = kx[q * 3 + 1];
-        sp_w[warp][0][2] = kx[q * 3 + 2];
-        si_w[warp][0] = ki[q];
-        sq_w[warp][0] = q;
-        if (warp == 0) {
-          order[k] = ki[q];  // fps_core.py:167-168
-          sel[k] = A::from_bits(kv[q]);
+        __syncwarp();
+        if (nct > 32) {
+          bits_t bv = A::kmin;
+          uint32_t bi = kNoIdx;
+          int bq = 0;
+          for (int q = lane; q < nb; q += 32)
+            if (kv[q] > bv || (kv[q] == bv && ki[q] < bi)) {
+              bv = kv[q];
+              bi = ki[q];
+              bq = q;
+            }
+          const int wl = argmax_lane_g<A>(bv, bi);
+          const int qmax = __shfl_sync(0xffffffffu, bq, wl);
+          if (lane == 0) top_w[0][0] = (int16_t)qmax;
+          nl = 1;
+          trunc = true;
+        } else {
+          const bool live = lane < nct;
+          const bits_t v = live ? cv_w[0][lane] : A::kmin;
+          const uint32_t i = live ? ci_w[0][lane] : kNoIdx;
+          int r3 = 0;
+#pragma unroll
+          for (int e = 0; e < 32; ++e) {
+            const bits_t ve = A::shfl(v, e);
+            const uint32_t ie = __shfl_sync(0xffffffffu, i, e);
+            r3 += (e < nct && (ve > v || (ve == v && ie < i))) ? 1 : 0;
+          }
+          if (live && r3 < KM) top_w[0][r3] = cq_w[0][lane];
+          nl = nct < KM ? nct : KM;
         }
       }
-      rmax = kv[q];
+      ncand_w = nct | (general ? 1 << 16 : 0);
+      if (trace) td[1] = td[2] = clock64();
+    }
+    __syncwarp();
+    // candidates in global rank order: lane < nc holds the lane-th
+    int nc;
+    bits_t cv = A::kmin, c2 = A::kmin;
+    T cx = T(0), cy = T(0), cz = T(0);
+    uint32_t cpos = kNoIdx;
+    int cq = -1;
+    if constexpr (CL == 1) {
+      nc = nl;
+      if (lane < nc) {
+        const int q = top_w[0][lane];
+        cv = kv[q]; c2 = k2[q]; cpos = ki[q]; cq = q;
+        cx = kx[q * 3 + 0]; cy = kx[q * 3 + 1]; cz = kx[q * 3 + 2];
+      }
     } else {
-      // rank of every list entry = number of larger keys (value desc, position asc)
-      for (int e = lane; e < ncand; e += 32) {
-        const bits_t v = rv_s[e];
-        const uint32_t i = ri_s[e];
-        int rank = 0;
-        for (int e2 = 0; e2 < ncand && rank < KM; ++e2) {
-          const bits_t v2 = rv_s[e2];
-          rank += (v2 > v || (v2 == v && ri_s[e2] < i)) ? 1 : 0;
+      const int par = round & 1;
+      const uint32_t buf = smem_u32(&xrec_s[par][0]);
+      {  // push the local list to every rank (lane = peer * KM + e)
+        const int peer = lane / KM, e = lane % KM;
+        if (peer < CL) {
+          const uint32_t dst = mapa(buf + (uint32_t)((rank * KM + e) * R::W * 4), (uint32_t)peer);
+          const uint32_t bar = mapa(smem_u32(&xbar_s[par]), (uint32_t)peer);
+          if (e < nl) {
+            const int q = top_w[0][e];
+            R::send(dst, bar, kv[q], k2[q], ki[q], q * CL + rank, kx[q * 3 + 0], kx[q * 3 + 1],
+                    kx[q * 3 + 2], trunc ? 1u : 0u);
+          } else {
+            R::send(dst, bar, A::kmin, A::kmin, kNoIdx, -1, T(0), T(0), T(0), 0u);
+          }
         }
-        if (rank < KM) top_w[warp][rank] = (int16_t)e;
       }
+      if (trace) td[3] = clock64();
+      mbar_wait(smem_u32(&xbar_s[par]), (uint32_t)((round >> 1) & 1));
+      if (trace) td[4] = clock64();
+      // merge the CL sorted lists: lane j holds record j, rank by shuffles
+      const uint32_t* rec = &xrec_s[par][0];
+      const int j = lane;
+      const bits_t vj = j < CL * KM ? R::v(rec + j * R::W) : A::kmin;
+      const uint32_t pj = j < CL * KM ? R::pos(rec + j * R::W) : kNoIdx;
+      const uint32_t fj = j < CL * KM ? R::flag(rec + j * R::W) : 0u;
+      const bool valid = vj != A::kmin;
+      int rk = 0;
+#pragma unroll
+      for (int i = 0; i < CL * KM; ++i) {
+        const bits_t vi = A::shfl(vj, i);
+        const uint32_t pi = __shfl_sync(0xffffffffu, pj, i);
+        rk += (vi != A::kmin && (vi > vj || (vi == vj && pi < pj))) ? 1 : 0;
+      }
+      // a truncated list is exact only up to its one record
+      const bool thead = valid && (j % KM) == 0 && fj != 0u;
+      const int limit = (int)__reduce_min_sync(0xffffffffu, thead ? (uint32_t)(rk + 1) : 32u);
+      const int nvalid = __popc(__ballot_sync(0xffffffffu, valid));
+      nc = nvalid < KM ? nvalid : KM;
+      nc = nc < limit ? nc : limit;
+      if (valid && rk < KM) top_w[0][rk] = (int16_t)j;
       __syncwarp();
-      const int nc = ncand < KM ? ncand : KM;
+      if (lane < nc) {
+        const uint32_t* r = rec + top_w[0][lane] * R::W;
+        cv = R::v(r); c2 = R::v2(r); cpos = R::pos(r); cq = R::q(r);
+        cx = R::c(r, 0); cy = R::c(r, 1); cz = R::c(r, 2);
+      }
+    }
+    if (trace) td[5] = clock64();
+    int acc;
+    {
+      // chain test (K1m): candidate j joins iff it is not closer than its own
+      // key to any earlier accepted candidate and beats their buckets' second best
       const bool live = lane < nc;
-      const int cand = live ? top_w[warp][lane] : 0;
-      const bits_t cv = live ? rv_s[cand] : A::kmin;
-      const bits_t c2 = live ? r2_s[cand] : A::kmin;
-      const T cx = live ? rx_s[cand][0] : T(0);
-      const T cy = live ? rx_s[cand][1] : T(0);
-      const T cz = live ? rx_s[cand][2] : T(0);
       bool ok = live && A::from_bits(cv) >= T(0);
+#pragma unroll
       for (int bb = 0; bb < KM - 1; ++bb) {
         const T bx = __shfl_sync(0xffffffffu, cx, bb);
         const T by = __shfl_sync(0xffffffffu, cy, bb);
         const T bz = __shfl_sync(0xffffffffu, cz, bb);
         const bits_t b2 = A::shfl(c2, bb);
-        if (bb < lane && ok)
-          ok = !(A::d2(cx, cy, cz, bx, by, bz) < A::from_bits(cv)) && cv > b2;  // (a), (b)
+        const bool cond = !(A::d2(cx, cy, cz, bx, by, bz) < A::from_bits(cv)) && cv > b2;  // (a), (b)
+        ok = ok && (bb >= lane || cond);
       }
       const unsigned okm = __ballot_sync(0xffffffffu, ok || lane == 0);
       acc = __ffs(~okm) - 1;
-      if (acc < 0 || acc > KM) acc = KM;
+      if (acc < 0 || acc > nc) acc = nc;
+      if (acc < 1) acc = 1;
       if (acc > iters - k) acc = iters - k;
       if (lane < acc) {
-        sp_w[warp][lane][0] = cx;
-        sp_w[warp][lane][1] = cy;
-        sp_w[warp][lane][2] = cz;
-        si_w[warp][lane] = ri_s[cand];
-        sq_w[warp][lane] = rq_s[cand];
-        if (warp == 0) {
-          order[k + lane] = ri_s[cand];  // fps_core.py:167-168
+        sp_w[0][lane][0] = cx;
+        sp_w[0][lane][1] = cy;
+        sp_w[0][lane][2] = cz;
+        si_w[0][lane] = cpos;
+        sq_w[0][lane] = cq;
+        if (rank == 0) {
+          order[k + lane] = cpos;  // fps_core.py:167-168
           sel[k + lane] = A::from_bits(cv);
         }
       }
-      rmax = A::shfl(cv, 0);
+      const bits_t r0 = A::shfl(cv, 0);
+      if (trace) td[6] = clock64();
+      if (lane == 0) {
+        acc_s = acc;
+        rmax_s = r0;
+      }
     }
-    __syncwarp();
+    }  // warp 0
+    __syncthreads();  // accepted points of the round visible to every warp
+    const int acc = acc_s;
+    rmax = rmax_s;
     J = acc;
     if (trace && round < prm.trace_iters) {
-      long long* rr = trace + (int64_t)round * 8;
+      long long* rr = trace + (int64_t)round * kTraceW;
       rr[0] = t0; rr[1] = t1; rr[2] = t2; rr[3] = t3; rr[4] = clock64(); rr[5] = acc;
-      rr[6] = nr; rr[7] = (long long)full | ((long long)nover << 1) | ((long long)ntest_w << 24);
+      rr[6] = nr | ((long long)ncand_w << 32); rr[7] = (long long)full | ((long long)ng << 1) | ((long long)ntest_w << 24);
+      for (int i = 0; i < 7; ++i) rr[8 + i] = td[i];
     }
     k += acc;
   }
 
+  if constexpr (CL > 1) cluster_sync_all();  // no rank leaves while peers may push into it
   // positions -> original indices for restricted runs (fps_cache.py:197)
-  if (prm.index_map != nullptr) {
+  if (prm.index_map != nullptr && rank == 0) {
     __syncthreads();
     const int64_t* map = prm.index_map + (int64_t)b * prm.map_stride;
     for (int kk = tid; kk < iters; kk += NT) order[kk] = __ldg(map + order[kk]);
   }
 }
 
-template <typename T, int PPL, int KM>
+template <typename T, int PPL, int KM, int CL>
 GridInst make_ginst() {
   GridInst k;
   k.dtype = sizeof(T) == 4 ? 0 : 1;
   k.nt = kBucketThreads;
   k.ppl = PPL;
   k.km = KM;
-  k.fn = reinterpret_cast<const void*>(&fps_grid_kernel<T, kBucketThreads, PPL, KM>);
+  k.cl = CL;
+  k.fn = reinterpret_cast<const void*>(&fps_grid_kernel<T, kBucketThreads, PPL, KM, CL>);
   k.esz = sizeof(T);
   return k;
 }
 
+#define FFPS_GRID_PPL(T, CL) \
+  make_ginst<T, 1, 8, CL>(), make_ginst<T, 2, 8, CL>(), make_ginst<T, 4, 8, CL>(), \
+      make_ginst<T, 8, 8, CL>()
+
 const GridInst* grid_instances(int* count) {
   static const GridInst insts[] = {
-      make_ginst<float, 1, 8>(),  make_ginst<float, 2, 8>(),  make_ginst<float, 4, 8>(),
-      make_ginst<float, 8, 8>(),  make_ginst<double, 1, 8>(), make_ginst<double, 2, 8>(),
-      make_ginst<double, 4, 8>(), make_ginst<double, 8, 8>(),
+      FFPS_GRID_PPL(float, 1),  FFPS_GRID_PPL(float, 2),  FFPS_GRID_PPL(float, 4),
+      FFPS_GRID_PPL(double, 1), FFPS_GRID_PPL(double, 2), FFPS_GRID_PPL(double, 4),
   };
   *count = (int)(sizeof(insts) / sizeof(insts[0]));
   return insts;
 }
 
-size_t grid_smem(int dtype, int64_t nb, int G) {
-  return dtype == 0 ? grid_smem_bytes<float>(nb, G) : grid_smem_bytes<double>(nb, G);
+size_t grid_smem(int dtype, int64_t nb) {
+  return dtype == 0 ? grid_smem_bytes<float>(nb) : grid_smem_bytes<double>(nb);
 }
 
 }  // namespace ffps

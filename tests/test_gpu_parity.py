@@ -16,13 +16,32 @@ from oracle import oracle
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(params=["stream", "bucket", "multi", "grid"])
+class _Sched:
+    """Run under one schedule: set_schedule(name); "grid@c" = K1g with c CTAs
+    per cloud, plain "grid" lets the library pick 1/2/4 from the batch."""
+
+    def __init__(self, name):
+        self.name = name
+
+    def __enter__(self):
+        from paper_2604_17720_b200 import _device
+        self.prev = _device.set_schedule(self.name)
+        return self
+
+    def __exit__(self, *exc):
+        from paper_2604_17720_b200 import _device
+        _device.set_schedule(self.prev)
+
+
+SCHEDULES = ["stream", "bucket", "multi", "grid", "grid@1", "grid@2"]
+
+
+@pytest.fixture(params=SCHEDULES)
 def schedule(request):
-    """Run the test under each greedy schedule (K1 streaming, K0+K1b bucketed)."""
-    from paper_2604_17720_b200 import _device
-    prev = _device.set_schedule(request.param)
-    yield request.param
-    _device.set_schedule(prev)
+    """Run the test under each greedy schedule (K1 streaming, K0+K1b bucketed,
+    K1m multi-winner, K1g cell-indexed with 1/2/4 CTAs per cloud)."""
+    with _Sched(request.param):
+        yield request.param
 
 
 # ---------------------------------------------------------------- golden (fp64)
@@ -261,14 +280,12 @@ def test_abi_rejects_bad_arguments(cuda):
     assert lib.ffps_fill_slice(0, 1, 1, 1, 10, 5, 4, None) == -1
 
 
-@pytest.mark.parametrize("sched", ["bucket", "multi", "grid"])
+@pytest.mark.parametrize("sched", ["bucket", "multi", "grid@1", "grid@2", "grid@4"])
 @pytest.mark.parametrize("dtype", [np.float32, np.float64])
 def test_bucketed_schedule_sizes_and_ties(cuda, dtype, sched):
-    """K0+K1b / K0+K1m forced on every size class: n below / at / above one
-    bucket, bucket sizes 32/64/128 (n up to 140K), heavy exact ties."""
-    from paper_2604_17720_b200 import _device
-    prev = _device.set_schedule(sched)
-    try:
+    """K0+K1b / K0+K1m / K1g forced on every size class: n below / at / above
+    one bucket, bucket sizes 32/64/128 (n up to 140K), heavy exact ties."""
+    with _Sched(sched):
         rng = np.random.default_rng(21)
         for N, m, B, kind in [(1, 1, 2, "uniform"), (31, 31, 2, "ties"), (32, 20, 2, "grid"),
                               (33, 33, 1, "collinear"), (1728, 900, 2, "grid"),
@@ -277,23 +294,17 @@ def test_bucketed_schedule_sizes_and_ties(cuda, dtype, sched):
             if kind == "grid":
                 N = min(N, 1728)
             _check_batch(_cloud(rng, B, N, kind, dtype), min(m, N), rng.integers(0, N, size=B))
-    finally:
-        _device.set_schedule(prev)
 
 
 @pytest.mark.parametrize("dtype", [np.float32, np.float64])
-@pytest.mark.parametrize("sched", ["multi", "grid"])
+@pytest.mark.parametrize("sched", ["multi", "grid@1", "grid@2", "grid@4"])
 def test_multi_winner_degenerate_ties(cuda, dtype, sched):
     """K1m when hundreds of bucket keys tie (identical points, exhausted
     buckets): the candidate list overflows and rounds fall back to one exact
     winner; results must still match the oracle."""
-    from paper_2604_17720_b200 import _device
-    prev = _device.set_schedule(sched)
-    try:
+    with _Sched(sched):
         rng = np.random.default_rng(23)
         for N, m in [(8000, 600), (20000, 3000)]:
             pts = np.zeros((2, N, 3))
             pts[:, : N // 50] = rng.random((2, N // 50, 3))  # 2% distinct, 98% duplicates
             _check_batch(np.ascontiguousarray(pts.astype(dtype)), m, np.array([0, N - 1]))
-    finally:
-        _device.set_schedule(prev)

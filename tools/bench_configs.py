@@ -41,13 +41,20 @@ def timeit(fn, warm, reps):
 
 
 def main():
-    clouds = sys.argv[1:] or ["uniform"]
-    for kind in clouds:
+    import argparse
+    ap = argparse.ArgumentParser()
+    ap.add_argument("clouds", nargs="*", default=["uniform"])
+    ap.add_argument("--scheds", nargs="*", default=["auto", "bucket", "grid", "stream"])
+    ap.add_argument("--configs", nargs="*", default=None, help="name prefixes, e.g. C5")
+    a = ap.parse_args()
+    for kind in a.clouds:
         for name, B, N, budgets, ps in CONFIGS:
             if kind == "lidar" and N < 100000:
                 continue
+            if a.configs and not any(name.startswith(c) for c in a.configs):
+                continue
             x = torch.from_numpy(bench.make_clouds(kind, B, N, 0)).cuda()
-            for sched in ("auto", "bucket", "grid", "stream"):
+            for sched in a.scheds:
                 prev = _device.set_schedule(sched)
                 try:
                     heavy = N >= 100000 and sched in ("stream", "bucket")

@@ -7,5 +7,4 @@ timeout 900 python bench.py --cloud lidar --no-cpu-baseline > gpurun_out/bench_l
 timeout 1500 python tools/bench_configs.py uniform lidar > gpurun_out/configs.jsonl 2> gpurun_out/configs.err; echo cfg=$?
 B2="python bench.py --steps 2 --warmup 1 --no-cpu-baseline --exh-steps 1"
 timeout 600 $B2 > gpurun_out/b2.log 2>&1 && timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv $B2 > gpurun_out/ncu_launch.log 2>&1; echo ncu1=$?
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:fps_bucket -c 1 -o gpurun_out/prof_bench_k1b $B2 > gpurun_out/ncu_full.log 2>&1; echo ncu2=$?
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:fps_greedy -c 1 -o gpurun_out/prof_bench_k1 $B2 > gpurun_out/ncu_full_k1.log 2>&1; echo ncu3=$?
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:fps_grid -c 1 -o gpurun_out/prof_bench_k1g $B2 > gpurun_out/ncu_full.log 2>&1; echo ncu2=$?

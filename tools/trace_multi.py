@@ -19,12 +19,20 @@ def main():
     ap.add_argument("--n", type=int, default=50000)
     ap.add_argument("--iters", type=int, default=12500)
     ap.add_argument("--nw", type=int, default=16)
-    ap.add_argument("--sched", default="multi", choices=["multi", "grid"])
+    ap.add_argument("--sched", default="multi",
+                    choices=["multi", "grid", "grid@1", "grid@2", "grid@4"])
+    ap.add_argument("--cloud", choices=["uniform", "lidar"], default="uniform")
+    ap.add_argument("--cloud-n", type=int, default=200000)
     a = ap.parse_args()
-    g = torch.Generator(device="cuda").manual_seed(0)
-    x = torch.rand((a.batch, a.n, 3), generator=g, device="cuda", dtype=torch.float64).float()
-    tr = torch.zeros((a.nw, a.iters, 8), dtype=torch.int64, device="cuda")
-    os.environ["FFPS_TRACE_MULTI" if a.sched == "multi" else "FFPS_TRACE_GRID"] = \
+    if a.cloud == "lidar":  # the bench's LiDAR frames, candidate prefix of n points
+        import bench
+        x = torch.from_numpy(bench.make_clouds("lidar", a.batch, a.cloud_n, 0)[:, :a.n].copy()).cuda()
+    else:
+        g = torch.Generator(device="cuda").manual_seed(0)
+        x = torch.rand((a.batch, a.n, 3), generator=g, device="cuda", dtype=torch.float64).float()
+    W = 16 if a.sched.startswith("grid") else 8
+    tr = torch.zeros((a.nw, a.iters, W), dtype=torch.int64, device="cuda")
+    os.environ["FFPS_TRACE_MULTI" if a.sched.startswith("multi") else "FFPS_TRACE_GRID"] = \
         f"{tr.data_ptr()},{a.iters}"
     prev = _device.set_schedule(a.sched)
     B = a.batch
@@ -40,23 +48,37 @@ def main():
     nsel = t[0, :, 5]
     print(f"rounds {R} for {a.iters} iterations: {nsel.sum() + 1} winners, "
           f"{(nsel.sum()) / R:.2f} per round")
-    names = (["bound", "reeval", "topk", "merge+barriers"] if a.sched == "multi" else
+    names = (["bound", "reeval", "topk", "merge+barriers"] if a.sched.startswith("multi") else
              ["flag", "reeval", "candidates", "merge+barriers"])
     ph = np.stack([t[:, :, i + 1] - t[:, :, i] for i in range(4)], -1)
     for lo, hi in [(1, max(2, R // 10)), (R // 10, R)]:
         sl = slice(lo, hi)
         tot = t[0, sl, 4] - t[0, sl, 0]
-        flagged = t[0, sl, 6] if a.sched == "grid" else t[:, sl, 6].sum(0)
-        if a.sched == "grid":
+        flagged = (t[0, sl, 6] & 0xffffffff) if a.sched.startswith("grid") else t[:, sl, 6].sum(0)
+        if a.sched.startswith("grid"):
             info = t[0, sl, 7]
-            print(f"   oversize buckets {(info[0] >> 1) & 0x7fffff}, cell entries per point "
-                  f"(warps with a point) {np.mean([((t[w, sl, 7] >> 24) / 2).mean() for w in range(t.shape[0])]):.1f}")
+            print(f"   candidates per round (warp 0) {(t[0, sl, 6] >> 32).mean():.1f}, "
+                  f"bucket groups {(info[0] >> 1) & 0x7fffff}, hit groups per warp-round "
+                  f"{np.mean([(t[w, sl, 7] >> 24).mean() for w in range(t.shape[0])]):.1f}")
         print(f"rounds [{lo},{hi}): cycles/round median {np.median(tot):.0f}, winners/round "
               f"{nsel[sl].mean():.2f}, flagged/round {flagged.mean():.1f}" +
-              (f", full-scan rounds {t[0, sl, 7].mean():.2f}" if a.sched == "grid" else ""))
+              (f", full-scan rounds {(t[0, sl, 7] & 1).mean():.2f}" if a.sched.startswith("grid") else ""))
         for i, nm in enumerate(names):
             v = ph[:, sl, i]
             print(f"   {nm:15s} mean {v.mean():7.0f}  max-warp mean {v.max(0).mean():7.0f}")
+        if W == 16:  # warp 0 sub-steps of phase D (0 = not reached / not traced)
+            d = t[0, sl, 8:15].astype(np.float64)
+            t3 = t[0, sl, 3].astype(np.float64)
+            marks = ["tau", "gather", "rank", "push", "wait", "merge", "chain"]
+            prev = t3
+            out = []
+            for i, m in enumerate(marks):
+                ok = d[:, i] > 0
+                if ok.any():
+                    out.append(f"{m} {np.median(d[ok, i] - prev[ok]):.0f}")
+                    prev = np.where(ok, d[:, i], prev)
+            out.append(f"tail {np.median(t[0, sl, 4] - prev):.0f}")
+            print("   D (warp 0, median cycles from the previous mark): " + ", ".join(out))
 
 
 if __name__ == "__main__":
