@@ -385,7 +385,7 @@ int run_bucketed(int dtype, const void* xyz, int64_t batch, int64_t cloud_stride
 }
 
 // K1g: smallest bucket size whose bucket table + cell index fit shared memory
-int grid_cluster(int algo, int64_t batch, int sms);
+int grid_cluster(int algo, int64_t batch, int sms, int64_t n);
 
 int run_grid(int dtype, const void* xyz, int64_t batch, int64_t cloud_stride, int64_t n,
              int64_t iters, const int64_t* seed_pos, const int64_t* index_map, int64_t map_stride,
@@ -395,8 +395,12 @@ int run_grid(int dtype, const void* xyz, int64_t batch, int64_t cloud_stride, in
   int cnt = 0;
   const ffps::GridInst* insts = ffps::grid_instances(&cnt);
   const ffps::GridInst* pick = nullptr;
-  const int km = 8;  // winners per round (KM = 16 measured 1.3-1.6x slower)
-  const int cl = grid_cluster(algo, batch, di.sms);  // CTAs per cloud
+  const int cl = grid_cluster(algo, batch, di.sms, n);  // CTAs per cloud
+  // winners per round at most: 16 (one DSMEM record per lane: CL * KM <= 32),
+  // 8 with 4 CTAs per cloud; FFPS_GRID_KM=8 forces 8
+  int km = cl <= 2 ? 16 : 8;
+  if (const char* v = getenv("FFPS_GRID_KM"))
+    if (atoi(v) == 8) km = 8;
   int64_t nb = 0;
   size_t smem = 0;
   for (int ppl = 1; ppl <= 8 && !pick; ppl *= 2) {
@@ -623,11 +627,13 @@ int resolve_algo(int algo, int64_t n, int64_t batch) {
 // CTAs per cloud of the grid schedule: fixed by the algo argument
 // (FFPS_ALGO_GRID_CL), else the largest of 1/2/4 with batch * c <= SMs;
 // FFPS_GRID_CL in the environment overrides both
-int grid_cluster(int algo, int64_t batch, int sms) {
+int grid_cluster(int algo, int64_t batch, int sms, int64_t n) {
   int cl = algo >> 8;
   if (cl == 0) {
+    // spread the batch over the SMs, but keep >= 512 buckets of 32 points per
+    // CTA: fewer leave too few bucket groups to hold KM candidates
     cl = 1;
-    while (cl < 4 && batch * (cl * 2) <= sms) cl *= 2;
+    while (cl < 4 && batch * (cl * 2) <= sms && (n + 31) / 32 >= 512 * (cl * 2)) cl *= 2;
   }
   if (const char* v = getenv("FFPS_GRID_CL")) {
     const int w = atoi(v);
@@ -681,7 +687,7 @@ int ffps_auto_schedule(int64_t n, int64_t batch) {
     cudaGetLastError();
     return a;
   }
-  return FFPS_ALGO_GRID_CL(grid_cluster(a, batch, device_info(dev).sms));
+  return FFPS_ALGO_GRID_CL(grid_cluster(a, batch, device_info(dev).sms, n));
 }
 
 int ffps_run_kernel_ex(int dtype, const void* xyz, int64_t batch, int64_t cloud_stride,

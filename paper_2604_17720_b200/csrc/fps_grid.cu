@@ -44,6 +44,28 @@ namespace {
 
 constexpr int kGS = 32;  // buckets per group of the two-level index (one per lane)
 constexpr int kTraceW = 16;  // trace words per round and warp (FFPS_TRACE_GRID)
+
+// flag phase: J points share the NW warps, wpp = NW / J warps per point;
+// warp w serves point t[J][w], part s[J][w] (a table instead of divisions)
+constexpr int kWppNW = 16, kWppJ = 16;
+struct WppTab {
+  unsigned char wpp[kWppJ + 1];
+  unsigned char t[kWppJ + 1][kWppNW];
+  unsigned char s[kWppJ + 1][kWppNW];
+};
+constexpr WppTab make_wpp_tab() {
+  WppTab w{};
+  for (int j = 1; j <= kWppJ; ++j) {
+    const int wpp = kWppNW / j;
+    w.wpp[j] = (unsigned char)wpp;
+    for (int x = 0; x < kWppNW; ++x) {
+      w.t[j][x] = (unsigned char)(x / wpp);
+      w.s[j][x] = (unsigned char)(x % wpp);
+    }
+  }
+  return w;
+}
+__constant__ WppTab c_wpp = make_wpp_tab();
 // rounds re-test every bucket while the search radius is this large a fraction
 // of the cloud's extent (little to prune, the whole CTA shares the work)
 constexpr double kFullFrac = 0.375;
@@ -77,7 +99,7 @@ __host__ __device__ constexpr size_t grid_smem_bytes(int64_t nb) {
   return (size_t)nb * (6 * sizeof(T) + 3 * sizeof(T) + 2 * sizeof(typename Arith<T>::bits_t) +
                        4 /*ki*/ + 4 /*pmask*/ + 4 /*rlist*/) +
          (size_t)((nb + kGS - 1) / kGS) *
-             (6 * sizeof(T) + 3 * sizeof(typename Arith<T>::bits_t) + 4 * 4);
+             (6 * sizeof(T) + 6 * sizeof(typename Arith<T>::bits_t) + 14 * 4);  // NCG <= 4
 }
 
 
@@ -143,6 +165,7 @@ __global__ void __launch_bounds__(NT, 1) fps_grid_kernel(const BucketParams prm)
   static_assert(NW >= KM, "KM warp maxima, at least one warp per point");
 
   static_assert(CL == 1 || CL == 2 || CL == 4, "cluster of 1, 2 or 4 CTAs");
+  static_assert(NW == kWppNW && KM <= kWppJ, "flag-phase table sized for 16 warps, J <= 16");
   static_assert(CL * KM <= 32, "one exchanged record per lane");
   using R = GridRec<T>;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -167,24 +190,28 @@ __global__ void __launch_bounds__(NT, 1) fps_grid_kernel(const BucketParams prm)
   T* kx = gbox + (size_t)ng * 6;                         // [nb][3] key point xyz
   bits_t* kv = reinterpret_cast<bits_t*>(kx + (size_t)nb * 3);  // [nb] key value
   bits_t* k2 = kv + nb;                                  // [nb] second-best value
-  // per group (phase C): best and second-best key (value, position, row), third value
+  // per group (phase C): max key, the (NCG+1)-th value; candidates NCG*g + k =
+  // the group's k-th best key (value, position, table row)
+  constexpr int NCG = KM / 4;  // candidates per group
   bits_t* gmax = k2 + nb;                                // [ng] group max key
-  bits_t* g2v = gmax + ng;                               // [ng]
-  bits_t* g3v = g2v + ng;                                // [ng]
-  uint32_t* ki = reinterpret_cast<uint32_t*>(g3v + ng);  // [nb] key position
+  bits_t* gnext = gmax + ng;                             // [ng]
+  bits_t* cand_v = gnext + ng;                           // [NCG ng]
+  uint32_t* ki = reinterpret_cast<uint32_t*>(cand_v + NCG * ng);  // [nb] key position
   uint32_t* pmask = ki + nb;                             // [nb] flagging points of the round
   int32_t* rlist = reinterpret_cast<int32_t*>(pmask + nb);  // [nb] round list
-  uint32_t* gp1 = reinterpret_cast<uint32_t*>(rlist + nb);  // [ng]
-  uint32_t* gp2 = gp1 + ng;                                 // [ng]
-  int32_t* gq1 = reinterpret_cast<int32_t*>(gp2 + ng);     // [ng] table row of the best
-  int32_t* gq2 = gq1 + ng;                                  // [ng]
-  constexpr int CPL = 8;  // candidates per lane in phase R (2 * ng <= 256)
+  uint32_t* cand_p = reinterpret_cast<uint32_t*>(rlist + nb);  // [NCG ng]
+  int32_t* cand_q = reinterpret_cast<int32_t*>(cand_p + NCG * ng);  // [NCG ng]
+  int32_t* gdirty = cand_q + NCG * ng;  // [ng] group has a re-evaluated bucket this round
+  int32_t* dlist = gdirty + ng;       // [ng] dirty groups
   // phase D: per-warp candidate list (<= 32)
   __shared__ bits_t cv_w[1][32];
   __shared__ uint32_t ci_w[1][32];
   __shared__ int16_t cq_w[1][32];
-  __shared__ int16_t top_s[KM];  // phase R: rows of the ranked top-KM candidates
+  __shared__ int16_t top_s[KM];  // rows of the ranked top-KM candidates
   __shared__ bits_t topv_s[KM];
+  __shared__ int topg_s[KM];     // the KM groups with the best maxima (phase R1)
+  __shared__ int ngv_s;          // non-empty groups (phase R1)
+  __shared__ int rr_s[64];       // phase R2 ranks (0x7fffffff: empty)
   // accepted points of the last round: every warp keeps its own copy (all
   // warps derive the same set from the candidate list, no barrier needed)
   __shared__ T sp_w[1][KM][3];
@@ -193,7 +220,8 @@ __global__ void __launch_bounds__(NT, 1) fps_grid_kernel(const BucketParams prm)
   __shared__ int16_t top_w[1][KM];
   __shared__ int acc_s;
   __shared__ bits_t rmax_s;
-  __shared__ int rcount_s;
+  __shared__ int rcount_s, npair_s, ndirty_s;
+  __shared__ int pair_s[KM * 128];  // flag phase: (point << 16 | group) pairs
   __shared__ T ext_s;
   __shared__ T red_s[2][NW][3];
   // CL > 1: incoming top lists [parity][rank * KM + e], one mbarrier per parity
@@ -228,7 +256,12 @@ __global__ void __launch_bounds__(NT, 1) fps_grid_kernel(const BucketParams prm)
       red_s[1][warp][c] = hi[c];
     }
   }
-  if (tid == 0) rcount_s = 0;
+  if (tid == 0) {
+    rcount_s = 0;
+    npair_s = 0;
+    ndirty_s = 0;
+    ngv_s = 0;
+  }
   __syncthreads();
   if (tid == 0) {
     T e = T(0);
@@ -258,9 +291,10 @@ __global__ void __launch_bounds__(NT, 1) fps_grid_kernel(const BucketParams prm)
       gbox[g * 6 + 3 + c] = z[c];
     }
     gmax[g] = A::bits(A::pinf());
+    gdirty[g] = 0;
   }
   __syncthreads();
-  const T full_r = (T)(kFullFrac * (double)ext_s);
+  const T full_r2 = (T)(kFullFrac * kFullFrac * (double)ext_s * (double)ext_s);
 
   // ---- seed (fps_core.py:124-130) -----------------------------------------------
   const int seed = (int)prm.seed_pos[b];
@@ -279,6 +313,7 @@ __global__ void __launch_bounds__(NT, 1) fps_grid_kernel(const BucketParams prm)
     order[0] = seed;
     sel[0] = A::pinf();
   }
+
   if constexpr (CL > 1) {
     if (tid == 0) {
       mbar_init(smem_u32(&xbar_s[0]), 1);
@@ -312,14 +347,16 @@ __global__ void __launch_bounds__(NT, 1) fps_grid_kernel(const BucketParams prm)
       int base = 0;
       if (lane == __ffs(m) - 1) base = atomicAdd(&rcount_s, __popc(m));
       base = __shfl_sync(0xffffffffu, base, __ffs(m) - 1);
-      if (isnew) rlist[base + __popc(m & ((1u << lane) - 1u))] = q;
+      if (isnew) {
+        rlist[base + __popc(m & ((1u << lane) - 1u))] = q;
+      }
     }
   };
 
   int k = 1;
   for (int round = 0; k < iters; ++round) {
     long long t0 = 0, t1 = 0, t2 = 0, t3 = 0;
-    long long td[7] = {0, 0, 0, 0, 0, 0, 0};  // warp 0: sub-steps of phase D
+    long long td[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // warp 0: sub-steps of phases R, D
     int ntest_w = 0;  // traced: hit groups of this warp
     int ncand_w = 0;  // traced: candidates of this warp
     if (trace) t0 = clock64();
@@ -329,8 +366,7 @@ __global__ void __launch_bounds__(NT, 1) fps_grid_kernel(const BucketParams prm)
     // A. flag ---------------------------------------------------------------------
     const T r2 = A::from_bits(rmax);
     // search radius: every key is <= R^2 (padded for the rounding of sqrt)
-    const T R = round == 0 ? A::pinf() : (T)(sqrt((double)r2) * 1.001);
-    const bool full = round == 0 || !(R < full_r);
+    const bool full = round == 0 || !(r2 < full_r2);
     if (full) {  // every bucket against every point
       for (int q = tid; q < nb; q += NT) {
         if (round == 0) {
@@ -343,33 +379,42 @@ __global__ void __launch_bounds__(NT, 1) fps_grid_kernel(const BucketParams prm)
           sq_w[0][lane] % CL == rank)
         flag(sq_w[0][lane] / CL, lane);  // the point -> -inf
     } else {
-      // wpp warps per selected point: test the group boxes against the group
-      // max keys (a group with box_d2 >= its max key holds no bucket the point
-      // can flag), then the kGS buckets of every hit group (one per lane)
-      const int wpp = NW / J;
+      // A1. wpp warps per selected point test the group boxes against the group
+      //     max keys (a group with box_d2 >= its max key holds no bucket the
+      //     point can flag); hits become (point, group) pairs
+      const int wpp = c_wpp.wpp[J];  // warps per point (NW = 16)
       if (warp < J * wpp) {
-        const int t = warp / wpp, sub = warp % wpp;
+        const int t = c_wpp.t[J][warp], sub = c_wpp.s[J][warp];
         const T px = sp_w[0][t][0], py = sp_w[0][t][1], pz = sp_w[0][t][2];
         for (int g0 = sub * 32; g0 < ng; g0 += wpp * 32) {
           const int g = g0 + lane;
           const bool hit = g < ng && !(box_lb(px, py, pz, gbox + (size_t)g * 6) >= A::from_bits(gmax[g]));
-          unsigned m = __ballot_sync(0xffffffffu, hit);
+          const unsigned m = __ballot_sync(0xffffffffu, hit);
           ntest_w += __popc(m);
-          while (m) {
-            const int q = (g0 + __ffs(m) - 1) * kGS + lane;
-            m &= m - 1u;
-            test_warp(q < nb, q < nb ? q : 0, t, px, py, pz);
+          if (m) {
+            int base = 0;
+            if (lane == __ffs(m) - 1) base = atomicAdd(&npair_s, __popc(m));
+            base = __shfl_sync(0xffffffffu, base, __ffs(m) - 1);
+            if (hit) pair_s[base + __popc(m & ((1u << lane) - 1u))] = (t << 16) | g;
           }
         }
         if (lane == 0 && sub == 0 && sq_w[0][t] >= 0 && sq_w[0][t] % CL == rank)
           flag(sq_w[0][t] / CL, t);  // the point -> -inf
+      }
+      __syncthreads();  // pair list complete
+      // A2. all warps: the kGS buckets of every pair (one per lane)
+      const int np = npair_s;
+      for (int e = warp; e < np; e += NW) {
+        const int pr = pair_s[e], t = pr >> 16;
+        const int q = (pr & 0xffff) * kGS + lane;
+        test_warp(q < nb, q < nb ? q : 0, t, sp_w[0][t][0], sp_w[0][t][1], sp_w[0][t][2]);
       }
     }
     if (trace) t1 = clock64();
     __syncthreads();  // flags and round list complete
     // B. re-evaluate the round list --------------------------------------------------
     const int nr = rcount_s;
-    auto batch = [&](auto chn, int e0) {
+    auto batch = [&](auto chn, int e0) {  // CH buckets e0, e0 + NW, ... in flight
       constexpr int CH = decltype(chn)::value;
       int qc[CH];
       uint32_t pm[CH];
@@ -438,81 +483,118 @@ __global__ void __launch_bounds__(NT, 1) fps_grid_kernel(const BucketParams prm)
           kx[q * 3 + 1] = y1;
           kx[q * 3 + 2] = z1;
           pmask[q] = 0u;
+          if (atomicExch(&gdirty[q / kGS], 1) == 0) dlist[atomicAdd(&ndirty_s, 1)] = q / kGS;
         }
       }
     };
     {
+      // all of a warp's buckets of the round in one batch when they fit
       constexpr int CH = PPL <= 1 ? 4 : (PPL == 2 ? 2 : 1);  // <= 4 points per lane in flight
-      int e = warp;
-      for (; e + (CH - 1) * NW < nr; e += CH * NW) batch(std::integral_constant<int, CH>{}, e);
-      for (; e < nr; e += NW) batch(std::integral_constant<int, 1>{}, e);
+      for (int e = warp; e < nr; e += CH * NW) {
+        const int nv = (nr - e + NW - 1) / NW;
+        if (nv >= CH) batch(std::integral_constant<int, CH>{}, e);
+        else if (CH >= 3 && nv == 3) batch(std::integral_constant<int, (CH >= 3 ? 3 : 1)>{}, e);
+        else if (CH >= 2 && nv == 2) batch(std::integral_constant<int, (CH >= 2 ? 2 : 1)>{}, e);
+        else batch(std::integral_constant<int, 1>{}, e);
+      }
     }
     if (trace) t2 = clock64();
     __syncthreads();  // keys final for this round
-    if (tid == 0) rcount_s = 0;
+    if (tid == 0) {
+      rcount_s = 0;
+      npair_s = 0;
+      ngv_s = 0;
+    }
     // C. group statistics (each warp refreshes a slice of whole groups, one
     //    bucket per lane): top-2 keys by (value desc, position asc) + third value
+    //    (only the groups with a re-evaluated bucket changed: the dirty list)
     {
-      const int gpw = (ng + NW - 1) / NW;
-      const int g_lo = warp * gpw, g_hi = g_lo + gpw < ng ? g_lo + gpw : ng;
-      for (int g = g_lo; g < g_hi; ++g) {
+      const int nd = ndirty_s;
+      for (int i = warp; i < nd; i += NW) {
+        const int g = dlist[i];
+        if (lane == 0) gdirty[g] = 0;
         const int q = g * kGS + lane;
         const bool in = q < nb;
         bits_t v = in ? kv[q] : A::kmin;
         const uint32_t p = in ? ki[q] : kNoIdx;
-        const bits_t m1 = A::warp_max(v);
-        const uint32_t p1 = __reduce_min_sync(0xffffffffu, v == m1 ? p : kNoIdx);
-        const unsigned w1 = __ballot_sync(0xffffffffu, v == m1 && p == p1);
-        if (w1 & (1u << lane)) v = A::kmin;
-        const bits_t m2 = A::warp_max(v);
-        const uint32_t p2 = __reduce_min_sync(0xffffffffu, v == m2 ? p : kNoIdx);
-        const unsigned w2 = __ballot_sync(0xffffffffu, v == m2 && p == p2) & ~w1;
-        if (w2 & (1u << lane)) v = A::kmin;
-        const bits_t m3 = A::warp_max(v);
-        if (lane == 0) {
-          gmax[g] = m1;
-          gp1[g] = p1;
-          gq1[g] = w1 ? g * kGS + __ffs(w1) - 1 : 0;
-          g2v[g] = m2;
-          gp2[g] = p2;
-          gq2[g] = w2 ? g * kGS + __ffs(w2) - 1 : 0;
-          g3v[g] = m3;
+        unsigned taken = 0u;
+#pragma unroll
+        for (int k = 0; k < NCG; ++k) {  // k-th best by (value desc, position asc)
+          const bits_t mk = A::warp_max(v);
+          const uint32_t pk = __reduce_min_sync(0xffffffffu, v == mk ? p : kNoIdx);
+          const unsigned wk = __ballot_sync(0xffffffffu, v == mk && p == pk) & ~taken;
+          taken |= wk;
+          if (wk & (1u << lane)) v = A::kmin;
+          if (lane == 0) {
+            if (k == 0) gmax[g] = mk;
+            cand_v[NCG * g + k] = mk;
+            cand_p[NCG * g + k] = pk;
+            cand_q[NCG * g + k] = wk ? g * kGS + __ffs(wk) - 1 : 0;
+          }
         }
+        const bits_t mn = A::warp_max(v);
+        if (lane == 0) gnext[g] = mn;
       }
     }
     if (trace) t3 = clock64();
     __syncthreads();  // group statistics final
-    // R. all warps: rank the candidates = the top-2 keys of every group
-    //    (candidate c: group c >> 1, slot c & 1).  Lane j of every warp holds
-    //    candidates j, j + 32, ...; warp w ranks c = w, w + NW, ... with one
-    //    ballot per lane slot; ranks < KM go to top_s (rows) / topv_s.
-    const int ncd = 2 * ng;
-    const int nj = (ncd + 31) / 32;
-    bits_t cvv[CPL];
-    uint32_t cpp[CPL];
+    if (tid == 0) ndirty_s = 0;
+    if (trace) td[0] = clock64();
+    // R1. all threads: rank of every group by its max key (value desc, position
+    //     asc), 16 threads per group; the KM best groups -> topg_s.  Every
+    //     top-KM key lies in those groups (a key elsewhere has KM group maxima
+    //     above it), and its rank among their candidates is its true rank.
+    {
+      const int gb = tid >> 4, part = tid & 15;
+      for (int g0 = 0; g0 < ng; g0 += NT / 16) {  // uniform trip count
+        const int g = g0 + gb;
+        const bits_t v = g < ng ? cand_v[NCG * g] : A::kmin;
+        const uint32_t p = g < ng ? cand_p[NCG * g] : kNoIdx;
+        int cnt = 0;
+        if (v != A::kmin)
+          for (int e = part; e < ng; e += 16) {
+            const bits_t ve = cand_v[NCG * e];
+            cnt += (ve > v || (ve == v && cand_p[NCG * e] < p)) ? 1 : 0;
+          }
 #pragma unroll
-    for (int j = 0; j < CPL; ++j) {
-      const int c = j * 32 + lane;
-      const bool in = j < nj && c < ncd;
-      cvv[j] = in ? ((c & 1) ? g2v[c >> 1] : gmax[c >> 1]) : A::kmin;
-      cpp[j] = in ? ((c & 1) ? gp2[c >> 1] : gp1[c >> 1]) : kNoIdx;
-    }
-    for (int c = warp; c < ncd; c += NW) {
-      const bits_t vc = (c & 1) ? g2v[c >> 1] : gmax[c >> 1];
-      if (vc == A::kmin) continue;
-      const uint32_t pc = (c & 1) ? gp2[c >> 1] : gp1[c >> 1];
-      int rk = 0;
-#pragma unroll
-      for (int j = 0; j < CPL; ++j) {
-        if (j >= nj) break;
-        rk += __popc(__ballot_sync(0xffffffffu, cvv[j] > vc || (cvv[j] == vc && cpp[j] < pc)));
-      }
-      if (lane == 0 && rk < KM) {
-        top_s[rk] = (int16_t)((c & 1) ? gq2[c >> 1] : gq1[c >> 1]);
-        topv_s[rk] = vc;
+        for (int o = 1; o < 16; o <<= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+        if (part == 0 && v != A::kmin) {
+          atomicAdd(&ngv_s, 1);
+          if (cnt < KM) topg_s[cnt] = g;
+        }
       }
     }
+    __syncthreads();  // group ranks final
+    // R2. all threads: ranks among the candidates of the top groups (<= KM * NCG
+    //     <= 64), 8 threads per candidate
+    const int ngt = ngv_s < KM ? ngv_s : KM;
+    const int nrc = ngt * NCG;
+    {
+      const int c = tid >> 3, part = tid & 7;
+      if (c < 64) {  // warps 0..15 all take part (NT = 512): uniform per warp
+        const int idx = c < nrc ? NCG * topg_s[c / NCG] + c % NCG : 0;
+        const bits_t v = c < nrc ? cand_v[idx] : A::kmin;
+        const uint32_t p = c < nrc ? cand_p[idx] : kNoIdx;
+        int cnt = 0;
+        if (v != A::kmin)
+          for (int e = part; e < nrc; e += 8) {
+            const int ie = NCG * topg_s[e / NCG] + e % NCG;
+            const bits_t ve = cand_v[ie];
+            cnt += (ve > v || (ve == v && cand_p[ie] < p)) ? 1 : 0;
+          }
+        cnt += __shfl_xor_sync(0xffffffffu, cnt, 1);
+        cnt += __shfl_xor_sync(0xffffffffu, cnt, 2);
+        cnt += __shfl_xor_sync(0xffffffffu, cnt, 4);
+        if (part == 0) rr_s[c] = v != A::kmin ? cnt : 0x7fffffff;
+        if (part == 0 && v != A::kmin && cnt < KM) {
+          top_s[cnt] = (int16_t)cand_q[idx];
+          topv_s[cnt] = v;
+        }
+      }
+    }
+    if (trace) td[1] = clock64();
     __syncthreads();  // candidate ranks final
+    if (trace) td[2] = clock64();
     // D. warp 0 alone: this rank's top-KM keys (table rows, rank order).
     //    tau2 = the KM-th candidate: a group whose third key reaches it may
     //    hold a top-KM key that is not a candidate -> the general path: every
@@ -524,16 +606,16 @@ __global__ void __launch_bounds__(NT, 1) fps_grid_kernel(const BucketParams prm)
     bool trunc = false;
     {
       const unsigned below = (1u << lane) - 1u;
+      // the ranked top-KM rows, tau2 = the KM-th candidate's value; a top group
+      // whose (NCG+1)-th key reaches tau2 may hold a top-KM key that is not a
+      // candidate -> the general path
       int nvalid = 0;
 #pragma unroll
-      for (int j = 0; j < CPL; ++j) nvalid += __popc(__ballot_sync(0xffffffffu, cvv[j] != A::kmin));
+      for (int c0 = 0; c0 < 64; c0 += 32)
+        nvalid += __popc(__ballot_sync(0xffffffffu, c0 + lane < nrc && rr_s[c0 + lane] != 0x7fffffff));
       const bits_t tau2 = nvalid >= KM ? topv_s[KM - 1] : A::kmin;
-      bool general = false;
-      for (int g0 = 0; g0 < ng; g0 += 32) {
-        const bits_t t3 = g0 + lane < ng ? g3v[g0 + lane] : A::kmin;
-        general |= __any_sync(0xffffffffu, t3 != A::kmin && t3 >= tau2);
-      }
-      if (trace) td[0] = clock64();
+      const bits_t tn = lane < ngt ? gnext[topg_s[lane]] : A::kmin;
+      const bool general = __any_sync(0xffffffffu, tn != A::kmin && tn >= tau2);
       int nct = nvalid;
       if (!general) {
         nl = nvalid < KM ? nvalid : KM;
@@ -592,7 +674,7 @@ __global__ void __launch_bounds__(NT, 1) fps_grid_kernel(const BucketParams prm)
         }
       }
       ncand_w = nct | (general ? 1 << 16 : 0);
-      if (trace) td[1] = td[2] = clock64();
+      if (trace) td[3] = clock64();
     }
     __syncwarp();
     // candidates in global rank order: lane < nc holds the lane-th
@@ -625,38 +707,62 @@ __global__ void __launch_bounds__(NT, 1) fps_grid_kernel(const BucketParams prm)
           }
         }
       }
-      if (trace) td[3] = clock64();
-      mbar_wait(smem_u32(&xbar_s[par]), (uint32_t)((round >> 1) & 1));
       if (trace) td[4] = clock64();
-      // merge the CL sorted lists: lane j holds record j, rank by shuffles
+      mbar_wait(smem_u32(&xbar_s[par]), (uint32_t)((round >> 1) & 1));
+      if (trace) td[5] = clock64();
+      // merge the CL sorted lists (value desc, position asc) with bitonic merge
+      // stages: lane l takes element e of list c = l / KM, odd lists reversed,
+      // so every pair of lists is a bitonic sequence (CL = 4: the upper half
+      // is reversed again before the final 2 * KM-wide merge)
       const uint32_t* rec = &xrec_s[par][0];
-      const int j = lane;
-      const bits_t vj = j < CL * KM ? R::v(rec + j * R::W) : A::kmin;
-      const uint32_t pj = j < CL * KM ? R::pos(rec + j * R::W) : kNoIdx;
-      const uint32_t fj = j < CL * KM ? R::flag(rec + j * R::W) : 0u;
-      const bool valid = vj != A::kmin;
-      int rk = 0;
-#pragma unroll
-      for (int i = 0; i < CL * KM; ++i) {
-        const bits_t vi = A::shfl(vj, i);
-        const uint32_t pi = __shfl_sync(0xffffffffu, pj, i);
-        rk += (vi != A::kmin && (vi > vj || (vi == vj && pi < pj))) ? 1 : 0;
+      int idx = -1;
+      bits_t mv = A::kmin;
+      uint32_t mp = kNoIdx;
+      if (lane < CL * KM) {
+        const int c = lane / KM, e = lane % KM;
+        idx = c * KM + ((c & 1) ? KM - 1 - e : e);
+        mv = R::v(rec + idx * R::W);
+        mp = R::pos(rec + idx * R::W);
       }
-      // a truncated list is exact only up to its one record
-      const bool thead = valid && (j % KM) == 0 && fj != 0u;
-      const int limit = (int)__reduce_min_sync(0xffffffffu, thead ? (uint32_t)(rk + 1) : 32u);
+      auto stage = [&](int j) {
+        const bits_t ov = __shfl_xor_sync(0xffffffffu, mv, j);
+        const uint32_t op = __shfl_xor_sync(0xffffffffu, mp, j);
+        const int oi = __shfl_xor_sync(0xffffffffu, idx, j);
+        const bool other_better = ov > mv || (ov == mv && op < mp);
+        const bool mine_better = mv > ov || (mv == ov && mp < op);
+        if ((lane & j) == 0 ? other_better : mine_better) {
+          mv = ov;
+          mp = op;
+          idx = oi;
+        }
+      };
+#pragma unroll
+      for (int j = KM; j > 0; j >>= 1) stage(j);
+      if constexpr (CL == 4) {
+        // lanes 16..31 hold the second sorted 16-list: reverse it, merge 32
+        const int src = lane < 2 * KM ? lane : 3 * 2 * KM - 1 - lane;
+        mv = A::shfl(mv, src);
+        mp = __shfl_sync(0xffffffffu, mp, src);
+        idx = __shfl_sync(0xffffffffu, idx, src);
+#pragma unroll
+        for (int j = 2 * KM; j > 0; j >>= 1) stage(j);
+      }
+      // lane r now holds the r-th record; a truncated list is exact only up to
+      // its one record (its head)
+      const bool valid = mv != A::kmin;
+      const bool thead = valid && (idx % KM) == 0 && R::flag(rec + idx * R::W) != 0u;
+      const unsigned th = __ballot_sync(0xffffffffu, thead);
+      const int limit = th ? __ffs(th) : 32;
       const int nvalid = __popc(__ballot_sync(0xffffffffu, valid));
       nc = nvalid < KM ? nvalid : KM;
       nc = nc < limit ? nc : limit;
-      if (valid && rk < KM) top_w[0][rk] = (int16_t)j;
-      __syncwarp();
       if (lane < nc) {
-        const uint32_t* r = rec + top_w[0][lane] * R::W;
-        cv = R::v(r); c2 = R::v2(r); cpos = R::pos(r); cq = R::q(r);
+        const uint32_t* r = rec + idx * R::W;
+        cv = mv; c2 = R::v2(r); cpos = mp; cq = R::q(r);
         cx = R::c(r, 0); cy = R::c(r, 1); cz = R::c(r, 2);
       }
     }
-    if (trace) td[5] = clock64();
+    if (trace) td[6] = clock64();
     int acc;
     {
       // chain test (K1m): candidate j joins iff it is not closer than its own
@@ -689,11 +795,12 @@ __global__ void __launch_bounds__(NT, 1) fps_grid_kernel(const BucketParams prm)
         }
       }
       const bits_t r0 = A::shfl(cv, 0);
-      if (trace) td[6] = clock64();
+      if (trace) td[7] = clock64();
       if (lane == 0) {
         acc_s = acc;
         rmax_s = r0;
       }
+
     }
     }  // warp 0
     __syncthreads();  // accepted points of the round visible to every warp
@@ -704,7 +811,7 @@ __global__ void __launch_bounds__(NT, 1) fps_grid_kernel(const BucketParams prm)
       long long* rr = trace + (int64_t)round * kTraceW;
       rr[0] = t0; rr[1] = t1; rr[2] = t2; rr[3] = t3; rr[4] = clock64(); rr[5] = acc;
       rr[6] = nr | ((long long)ncand_w << 32); rr[7] = (long long)full | ((long long)ng << 1) | ((long long)ntest_w << 24);
-      for (int i = 0; i < 7; ++i) rr[8 + i] = td[i];
+      for (int i = 0; i < 8; ++i) rr[8 + i] = td[i];
     }
     k += acc;
   }
@@ -731,14 +838,16 @@ GridInst make_ginst() {
   return k;
 }
 
-#define FFPS_GRID_PPL(T, CL) \
-  make_ginst<T, 1, 8, CL>(), make_ginst<T, 2, 8, CL>(), make_ginst<T, 4, 8, CL>(), \
-      make_ginst<T, 8, 8, CL>()
+#define FFPS_GRID_PPL(T, KM, CL) \
+  make_ginst<T, 1, KM, CL>(), make_ginst<T, 2, KM, CL>(), make_ginst<T, 4, KM, CL>(), \
+      make_ginst<T, 8, KM, CL>()
 
 const GridInst* grid_instances(int* count) {
   static const GridInst insts[] = {
-      FFPS_GRID_PPL(float, 1),  FFPS_GRID_PPL(float, 2),  FFPS_GRID_PPL(float, 4),
-      FFPS_GRID_PPL(double, 1), FFPS_GRID_PPL(double, 2), FFPS_GRID_PPL(double, 4),
+      FFPS_GRID_PPL(float, 8, 1),   FFPS_GRID_PPL(float, 8, 2),   FFPS_GRID_PPL(float, 8, 4),
+      FFPS_GRID_PPL(double, 8, 1),  FFPS_GRID_PPL(double, 8, 2),  FFPS_GRID_PPL(double, 8, 4),
+      FFPS_GRID_PPL(float, 16, 1),  FFPS_GRID_PPL(float, 16, 2),  FFPS_GRID_PPL(double, 16, 1),
+      FFPS_GRID_PPL(double, 16, 2),
   };
   *count = (int)(sizeof(insts) / sizeof(insts[0]));
   return insts;

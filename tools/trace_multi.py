@@ -67,9 +67,9 @@ def main():
             v = ph[:, sl, i]
             print(f"   {nm:15s} mean {v.mean():7.0f}  max-warp mean {v.max(0).mean():7.0f}")
         if W == 16:  # warp 0 sub-steps of phase D (0 = not reached / not traced)
-            d = t[0, sl, 8:15].astype(np.float64)
+            d = t[0, sl, 8:16].astype(np.float64)
             t3 = t[0, sl, 3].astype(np.float64)
-            marks = ["tau", "gather", "rank", "push", "wait", "merge", "chain"]
+            marks = ["B3", "R", "B4", "select", "push", "wait", "merge", "chain"]
             prev = t3
             out = []
             for i, m in enumerate(marks):
