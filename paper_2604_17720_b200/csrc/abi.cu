@@ -396,8 +396,10 @@ int run_grid(int dtype, const void* xyz, int64_t batch, int64_t cloud_stride, in
   const ffps::GridInst* insts = ffps::grid_instances(&cnt);
   const ffps::GridInst* pick = nullptr;
   const int cl = grid_cluster(algo, batch, di.sms, n);  // CTAs per cloud
-  // winners per round at most: 16 (one DSMEM record per lane: CL * KM <= 32),
-  // 8 with 4 CTAs per cloud; FFPS_GRID_KM=8 forces 8
+  // winners per round at most: 16 with 1-2 CTAs per cloud (one DSMEM record
+  // per lane: CL * KM <= 32), 8 with 4 CTAs per cloud; FFPS_GRID_KM=8 forces 8.
+  // (KM = 32 — the kernel template supports it for 1-2 CTAs — was measured
+  // slower at C5: 21 winners per round but 20K cycles per round.)
   int km = cl <= 2 ? 16 : 8;
   if (const char* v = getenv("FFPS_GRID_KM"))
     if (atoi(v) == 8) km = 8;
@@ -408,11 +410,16 @@ int run_grid(int dtype, const void* xyz, int64_t batch, int64_t cloud_stride, in
     const int64_t nbl = (nb + cl - 1) / cl;  // buckets of cluster rank 0 (the most)
     if (nbl > 4096) continue;                 // <= 128 bucket groups per CTA
     smem = ffps::grid_smem(dtype, nbl);
-    if (smem + 20480 > di.smem_optin) continue;  // + static shared memory
     for (int i = 0; i < cnt; ++i)
       if (insts[i].dtype == dtype && insts[i].ppl == ppl && insts[i].km == km &&
-          insts[i].cl == cl)
-        pick = &insts[i];
+          insts[i].cl == cl) {
+        cudaFuncAttributes fa;
+        if (cudaFuncGetAttributes(&fa, insts[i].fn) != cudaSuccess) {
+          cudaGetLastError();
+          continue;
+        }
+        if (smem + fa.sharedSizeBytes <= di.smem_optin) pick = &insts[i];  // + static smem
+      }
   }
   if (!pick) return fail(FFPS_EUNSUPPORTED, "no grid configuration for n=%lld", (long long)n);
   const int64_t bs = 32 * pick->ppl;

@@ -44,6 +44,7 @@ namespace {
 
 constexpr int kGS = 32;  // buckets per group of the two-level index (one per lane)
 constexpr int kTraceW = 16;  // trace words per round and warp (FFPS_TRACE_GRID)
+constexpr int kMaxGW = 4;    // dirty-group mask words: <= 128 bucket groups per CTA (host)
 
 // flag phase: J points share the NW warps, wpp = NW / J warps per point;
 // warp w serves point t[J][w], part s[J][w] (a table instead of divisions)
@@ -162,11 +163,11 @@ __global__ void __launch_bounds__(NT, 1) fps_grid_kernel(const BucketParams prm)
   constexpr int BS = 32 * PPL;
   constexpr uint32_t kNoIdx = 0xffffffffu;
   static_assert(KM <= 32, "one candidate per lane in the chain test");
-  static_assert(NW >= KM, "KM warp maxima, at least one warp per point");
 
   static_assert(CL == 1 || CL == 2 || CL == 4, "cluster of 1, 2 or 4 CTAs");
-  static_assert(NW == kWppNW && KM <= kWppJ, "flag-phase table sized for 16 warps, J <= 16");
-  static_assert(CL * KM <= 32, "one exchanged record per lane");
+  static_assert(NW == kWppNW, "flag-phase table sized for 16 warps");
+  static_assert(CL * KM <= 32 || (CL == 2 && KM == 32),
+                "one exchanged record per lane, or two lists of 32 (half-cleaner in lane)");
   using R = GridRec<T>;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int rank = CL > 1 ? (int)cluster_ctarank() : 0;
@@ -192,7 +193,7 @@ __global__ void __launch_bounds__(NT, 1) fps_grid_kernel(const BucketParams prm)
   bits_t* k2 = kv + nb;                                  // [nb] second-best value
   // per group (phase C): max key, the (NCG+1)-th value; candidates NCG*g + k =
   // the group's k-th best key (value, position, table row)
-  constexpr int NCG = KM / 4;  // candidates per group
+  constexpr int NCG = KM <= 16 ? KM / 4 : 4;  // candidates per group
   bits_t* gmax = k2 + nb;                                // [ng] group max key
   bits_t* gnext = gmax + ng;                             // [ng]
   bits_t* cand_v = gnext + ng;                           // [NCG ng]
@@ -204,14 +205,20 @@ __global__ void __launch_bounds__(NT, 1) fps_grid_kernel(const BucketParams prm)
   int32_t* gdirty = cand_q + NCG * ng;  // [ng] group has a re-evaluated bucket this round
   int32_t* dlist = gdirty + ng;       // [ng] dirty groups
   // phase D: per-warp candidate list (<= 32)
-  __shared__ bits_t cv_w[1][32];
-  __shared__ uint32_t ci_w[1][32];
-  __shared__ int16_t cq_w[1][32];
+  __shared__ bits_t cv_w[1][64];
+  __shared__ uint32_t ci_w[1][64];
+  __shared__ int16_t cq_w[1][64];
   __shared__ int16_t top_s[KM];  // rows of the ranked top-KM candidates
   __shared__ bits_t topv_s[KM];
   __shared__ int topg_s[KM];     // the KM groups with the best maxima (phase R1)
   __shared__ int ngv_s;          // non-empty groups (phase R1)
-  __shared__ int rr_s[64];       // phase R2 ranks (0x7fffffff: empty)
+  __shared__ int rr_s[KM * NCG];  // phase R2 ranks (0x7fffffff: empty)
+  // phase R1 -> R2: the candidates of the top-KM groups, group rank major
+  // (empty entries: value kmin), so R2 reads them without indirection
+  __shared__ bits_t compv_s[KM * NCG];
+  __shared__ uint32_t compp_s[KM * NCG];
+  __shared__ int compq_s[KM * NCG];
+  __shared__ unsigned dmask_s[kMaxGW];  // groups with a re-evaluated bucket this round
   // accepted points of the last round: every warp keeps its own copy (all
   // warps derive the same set from the candidate list, no barrier needed)
   __shared__ T sp_w[1][KM][3];
@@ -262,6 +269,7 @@ __global__ void __launch_bounds__(NT, 1) fps_grid_kernel(const BucketParams prm)
     ndirty_s = 0;
     ngv_s = 0;
   }
+  if (tid < kMaxGW) dmask_s[tid] = 0u;
   __syncthreads();
   if (tid == 0) {
     T e = T(0);
@@ -336,20 +344,39 @@ __global__ void __launch_bounds__(NT, 1) fps_grid_kernel(const BucketParams prm)
   auto test = [&](int q, int t, T px, T py, T pz) {  // K1b's exact bound test
     if (!(box_lb(px, py, pz, box + (size_t)q * 6) >= A::from_bits(kv[q]))) flag(q, t);
   };
-  // warp-converged variant: every lane calls it (valid = has a bucket to test);
-  // new buckets are appended with one shared-memory atomic per warp
-  auto test_warp = [&](bool valid, int q, int t, T px, T py, T pz) {
-    bool isnew = false;
-    if (valid && !(box_lb(px, py, pz, box + (size_t)q * 6) >= A::from_bits(kv[q])))
-      isnew = atomicOr(&pmask[q], 1u << t) == 0u;
-    const unsigned m = __ballot_sync(0xffffffffu, isnew);
-    if (m) {
-      int base = 0;
-      if (lane == __ffs(m) - 1) base = atomicAdd(&rcount_s, __popc(m));
-      base = __shfl_sync(0xffffffffu, base, __ffs(m) - 1);
-      if (isnew) {
-        rlist[base + __popc(m & ((1u << lane) - 1u))] = q;
+  // warp-converged variant for two (point, bucket) tests per lane (two pairs of
+  // the flag phase in flight): every lane calls it; new buckets are appended
+  // with one shared-memory atomic per warp and their points prefetched to L1
+  auto test_warp2 = [&](bool v0, int q0, int t0, bool v1, int q1, int t1) {
+    const bool h0 = v0 && !(box_lb(sp_w[0][t0][0], sp_w[0][t0][1], sp_w[0][t0][2],
+                                   box + (size_t)q0 * 6) >= A::from_bits(kv[q0]));
+    const bool h1 = v1 && !(box_lb(sp_w[0][t1][0], sp_w[0][t1][1], sp_w[0][t1][2],
+                                   box + (size_t)q1 * 6) >= A::from_bits(kv[q1]));
+    const bool n0 = h0 && atomicOr(&pmask[q0], 1u << t0) == 0u;
+    const bool n1 = h1 && atomicOr(&pmask[q1], 1u << t1) == 0u;
+    auto prefetch = [&](int q) {  // re-evaluated after the barrier: start its L2 -> L1 fill
+      const int64_t s0 = ((int64_t)q * CL + rank) * BS;
+#pragma unroll
+      for (int u = 0; u < BS * (int)sizeof(T) / 128; ++u) {
+        prefetch_l1(X + s0 + u * (128 / sizeof(T)));
+        prefetch_l1(Y + s0 + u * (128 / sizeof(T)));
+        prefetch_l1(Z + s0 + u * (128 / sizeof(T)));
+        prefetch_l1(D + s0 + u * (128 / sizeof(T)));
       }
+#pragma unroll
+      for (int u = 0; u < BS * 4 / 128; ++u) prefetch_l1(O + s0 + u * 32);
+    };
+    if (n0) prefetch(q0);
+    if (n1) prefetch(q1);
+    const unsigned m0 = __ballot_sync(0xffffffffu, n0), m1 = __ballot_sync(0xffffffffu, n1);
+    if (m0 | m1) {
+      const int c0 = __popc(m0);
+      int base = 0;
+      if (lane == 0) base = atomicAdd(&rcount_s, c0 + __popc(m1));
+      base = __shfl_sync(0xffffffffu, base, 0);
+      const unsigned below = (1u << lane) - 1u;
+      if (n0) rlist[base + __popc(m0 & below)] = q0;
+      if (n1) rlist[base + c0 + __popc(m1 & below)] = q1;
     }
   };
 
@@ -382,9 +409,11 @@ __global__ void __launch_bounds__(NT, 1) fps_grid_kernel(const BucketParams prm)
       // A1. wpp warps per selected point test the group boxes against the group
       //     max keys (a group with box_d2 >= its max key holds no bucket the
       //     point can flag); hits become (point, group) pairs
-      const int wpp = c_wpp.wpp[J];  // warps per point (NW = 16)
-      if (warp < J * wpp) {
-        const int t = c_wpp.t[J][warp], sub = c_wpp.s[J][warp];
+      // (J > 16: one warp per point, warp w takes points w, w + 16)
+      const int wpp = J <= kWppJ ? c_wpp.wpp[J] : 1;  // warps per point (NW = 16)
+#pragma unroll 1
+      for (int tw = warp; tw < (J <= kWppJ ? J * wpp : J); tw += NW) {
+        const int t = J <= kWppJ ? c_wpp.t[J][tw] : tw, sub = J <= kWppJ ? c_wpp.s[J][tw] : 0;
         const T px = sp_w[0][t][0], py = sp_w[0][t][1], pz = sp_w[0][t][2];
         for (int g0 = sub * 32; g0 < ng; g0 += wpp * 32) {
           const int g = g0 + lane;
@@ -404,10 +433,12 @@ __global__ void __launch_bounds__(NT, 1) fps_grid_kernel(const BucketParams prm)
       __syncthreads();  // pair list complete
       // A2. all warps: the kGS buckets of every pair (one per lane)
       const int np = npair_s;
-      for (int e = warp; e < np; e += NW) {
-        const int pr = pair_s[e], t = pr >> 16;
-        const int q = (pr & 0xffff) * kGS + lane;
-        test_warp(q < nb, q < nb ? q : 0, t, sp_w[0][t][0], sp_w[0][t][1], sp_w[0][t][2]);
+      for (int e = warp; e < np; e += 2 * NW) {
+        const bool two = e + NW < np;
+        const int pr0 = pair_s[e], pr1 = two ? pair_s[e + NW] : pr0;
+        const int q0 = (pr0 & 0xffff) * kGS + lane, q1 = (pr1 & 0xffff) * kGS + lane;
+        test_warp2(q0 < nb, q0 < nb ? q0 : 0, pr0 >> 16, two && q1 < nb, q1 < nb ? q1 : 0,
+                   pr1 >> 16);
       }
     }
     if (trace) t1 = clock64();
@@ -483,7 +514,7 @@ __global__ void __launch_bounds__(NT, 1) fps_grid_kernel(const BucketParams prm)
           kx[q * 3 + 1] = y1;
           kx[q * 3 + 2] = z1;
           pmask[q] = 0u;
-          if (atomicExch(&gdirty[q / kGS], 1) == 0) dlist[atomicAdd(&ndirty_s, 1)] = q / kGS;
+          atomicOr(&dmask_s[(q / kGS) >> 5], 1u << ((q / kGS) & 31));
         }
       }
     };
@@ -508,11 +539,15 @@ __global__ void __launch_bounds__(NT, 1) fps_grid_kernel(const BucketParams prm)
     // C. group statistics (each warp refreshes a slice of whole groups, one
     //    bucket per lane): top-2 keys by (value desc, position asc) + third value
     //    (only the groups with a re-evaluated bucket changed: the dirty list)
-    {
-      const int nd = ndirty_s;
-      for (int i = warp; i < nd; i += NW) {
-        const int g = dlist[i];
-        if (lane == 0) gdirty[g] = 0;
+    if (tid < KM * NCG) compv_s[tid] = A::kmin;  // R1 fills the ranks it finds
+    for (int wd = 0, base = 0; wd < ((ng + 31) >> 5); ++wd) {
+      const unsigned mword = dmask_s[wd];
+      const int cw = __popc(mword);
+      // lane l holds bit l of the word and its rank among the set bits
+      const bool bit = (mword >> lane) & 1u;
+      const int brank = __popc(mword & ((1u << lane) - 1u));
+      for (int j = ((warp - base) % NW + NW) % NW; j < cw; j += NW) {
+        const int g = wd * 32 + __ffs(__ballot_sync(0xffffffffu, bit && brank == j)) - 1;
         const int q = g * kGS + lane;
         const bool in = q < nb;
         bits_t v = in ? kv[q] : A::kmin;
@@ -535,10 +570,11 @@ __global__ void __launch_bounds__(NT, 1) fps_grid_kernel(const BucketParams prm)
         const bits_t mn = A::warp_max(v);
         if (lane == 0) gnext[g] = mn;
       }
+      base += cw;
     }
     if (trace) t3 = clock64();
     __syncthreads();  // group statistics final
-    if (tid == 0) ndirty_s = 0;
+    if (tid < kMaxGW) dmask_s[tid] = 0u;
     if (trace) td[0] = clock64();
     // R1. all threads: rank of every group by its max key (value desc, position
     //     asc), 16 threads per group; the KM best groups -> topg_s.  Every
@@ -560,34 +596,43 @@ __global__ void __launch_bounds__(NT, 1) fps_grid_kernel(const BucketParams prm)
         for (int o = 1; o < 16; o <<= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
         if (part == 0 && v != A::kmin) {
           atomicAdd(&ngv_s, 1);
-          if (cnt < KM) topg_s[cnt] = g;
+          if (cnt < KM) {
+            topg_s[cnt] = g;
+#pragma unroll
+            for (int k = 0; k < NCG; ++k) {
+              compv_s[cnt * NCG + k] = cand_v[NCG * g + k];
+              compp_s[cnt * NCG + k] = cand_p[NCG * g + k];
+              compq_s[cnt * NCG + k] = cand_q[NCG * g + k];
+            }
+          }
         }
       }
     }
     __syncthreads();  // group ranks final
     // R2. all threads: ranks among the candidates of the top groups (<= KM * NCG
-    //     <= 64), 8 threads per candidate
+    //     <= 64, compacted by R1), 8 threads per candidate
     const int ngt = ngv_s < KM ? ngv_s : KM;
     const int nrc = ngt * NCG;
     {
-      const int c = tid >> 3, part = tid & 7;
-      if (c < 64) {  // warps 0..15 all take part (NT = 512): uniform per warp
-        const int idx = c < nrc ? NCG * topg_s[c / NCG] + c % NCG : 0;
-        const bits_t v = c < nrc ? cand_v[idx] : A::kmin;
-        const uint32_t p = c < nrc ? cand_p[idx] : kNoIdx;
+      constexpr int NC = KM * NCG;
+      constexpr int TPC = NT / NC >= 8 ? 8 : NT / NC;  // threads per candidate
+      static_assert(TPC >= 1 && NC % TPC == 0, "R2 layout");
+      const int c = tid / TPC, part = tid % TPC;
+      if (c < NC) {  // whole warps (NC is a multiple of 4)
+        const bits_t v = compv_s[c];
+        const uint32_t p = compp_s[c];
         int cnt = 0;
-        if (v != A::kmin)
-          for (int e = part; e < nrc; e += 8) {
-            const int ie = NCG * topg_s[e / NCG] + e % NCG;
-            const bits_t ve = cand_v[ie];
-            cnt += (ve > v || (ve == v && cand_p[ie] < p)) ? 1 : 0;
-          }
-        cnt += __shfl_xor_sync(0xffffffffu, cnt, 1);
-        cnt += __shfl_xor_sync(0xffffffffu, cnt, 2);
-        cnt += __shfl_xor_sync(0xffffffffu, cnt, 4);
+#pragma unroll
+        for (int i = 0; i < NC / TPC; ++i) {  // empty entries (kmin) never rank above
+          const bits_t ve = compv_s[part + TPC * i];
+          const uint32_t pe = compp_s[part + TPC * i];
+          cnt += (ve > v || (ve == v && pe < p)) ? 1 : 0;
+        }
+#pragma unroll
+        for (int o = 1; o < TPC; o <<= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
         if (part == 0) rr_s[c] = v != A::kmin ? cnt : 0x7fffffff;
         if (part == 0 && v != A::kmin && cnt < KM) {
-          top_s[cnt] = (int16_t)cand_q[idx];
+          top_s[cnt] = (int16_t)compq_s[c];
           topv_s[cnt] = v;
         }
       }
@@ -611,7 +656,7 @@ __global__ void __launch_bounds__(NT, 1) fps_grid_kernel(const BucketParams prm)
       // candidate -> the general path
       int nvalid = 0;
 #pragma unroll
-      for (int c0 = 0; c0 < 64; c0 += 32)
+      for (int c0 = 0; c0 < KM * NCG; c0 += 32)
         nvalid += __popc(__ballot_sync(0xffffffffu, c0 + lane < nrc && rr_s[c0 + lane] != 0x7fffffff));
       const bits_t tau2 = nvalid >= KM ? topv_s[KM - 1] : A::kmin;
       const bits_t tn = lane < ngt ? gnext[topg_s[lane]] : A::kmin;
@@ -634,7 +679,7 @@ __global__ void __launch_bounds__(NT, 1) fps_grid_kernel(const BucketParams prm)
             const bool c = v >= tau2 && v != A::kmin;
             const unsigned cm = __ballot_sync(0xffffffffu, c);
             const int slot = nct + __popc(cm & below);
-            if (c && slot < 32) {
+            if (c && slot < 64) {
               cv_w[0][slot] = v;
               ci_w[0][slot] = ki[q];
               cq_w[0][slot] = (int16_t)q;
@@ -643,7 +688,7 @@ __global__ void __launch_bounds__(NT, 1) fps_grid_kernel(const BucketParams prm)
           }
         }
         __syncwarp();
-        if (nct > 32) {
+        if (nct > 64) {
           bits_t bv = A::kmin;
           uint32_t bi = kNoIdx;
           int bq = 0;
@@ -659,17 +704,19 @@ __global__ void __launch_bounds__(NT, 1) fps_grid_kernel(const BucketParams prm)
           nl = 1;
           trunc = true;
         } else {
-          const bool live = lane < nct;
-          const bits_t v = live ? cv_w[0][lane] : A::kmin;
-          const uint32_t i = live ? ci_w[0][lane] : kNoIdx;
-          int r3 = 0;
 #pragma unroll
-          for (int e = 0; e < 32; ++e) {
-            const bits_t ve = A::shfl(v, e);
-            const uint32_t ie = __shfl_sync(0xffffffffu, i, e);
-            r3 += (e < nct && (ve > v || (ve == v && ie < i))) ? 1 : 0;
+          for (int h = 0; h < 2; ++h) {  // entries lane and lane + 32
+            const int x = lane + 32 * h;
+            const bool live = x < nct;
+            const bits_t v = live ? cv_w[0][x] : A::kmin;
+            const uint32_t i = live ? ci_w[0][x] : kNoIdx;
+            int r3 = 0;
+            for (int e = 0; e < nct; ++e) {
+              const bits_t ve = cv_w[0][e];
+              r3 += (ve > v || (ve == v && ci_w[0][e] < i)) ? 1 : 0;
+            }
+            if (live && r3 < KM) top_w[0][r3] = cq_w[0][x];
           }
-          if (live && r3 < KM) top_w[0][r3] = cq_w[0][lane];
           nl = nct < KM ? nct : KM;
         }
       }
@@ -693,9 +740,10 @@ __global__ void __launch_bounds__(NT, 1) fps_grid_kernel(const BucketParams prm)
     } else {
       const int par = round & 1;
       const uint32_t buf = smem_u32(&xrec_s[par][0]);
-      {  // push the local list to every rank (lane = peer * KM + e)
-        const int peer = lane / KM, e = lane % KM;
-        if (peer < CL) {
+#pragma unroll
+      for (int r = lane; r < CL * KM; r += 32) {  // push the local list to every rank
+        const int peer = r / KM, e = r % KM;
+        {
           const uint32_t dst = mapa(buf + (uint32_t)((rank * KM + e) * R::W * 4), (uint32_t)peer);
           const uint32_t bar = mapa(smem_u32(&xbar_s[par]), (uint32_t)peer);
           if (e < nl) {
@@ -718,7 +766,17 @@ __global__ void __launch_bounds__(NT, 1) fps_grid_kernel(const BucketParams prm)
       int idx = -1;
       bits_t mv = A::kmin;
       uint32_t mp = kNoIdx;
-      if (lane < CL * KM) {
+      if constexpr (CL * KM == 64) {
+        // two lists of 32: lane l compares element l of list 0 with element
+        // 31 - l of list 1 (half-cleaner); the better 32 form a bitonic sequence
+        const int ia = lane, ib = KM + KM - 1 - lane;
+        const bits_t va = R::v(rec + ia * R::W), vb = R::v(rec + ib * R::W);
+        const uint32_t pa = R::pos(rec + ia * R::W), pb = R::pos(rec + ib * R::W);
+        const bool a_better = va > vb || (va == vb && pa < pb);
+        idx = a_better ? ia : ib;
+        mv = a_better ? va : vb;
+        mp = a_better ? pa : pb;
+      } else if (lane < CL * KM) {
         const int c = lane / KM, e = lane % KM;
         idx = c * KM + ((c & 1) ? KM - 1 - e : e);
         mv = R::v(rec + idx * R::W);
@@ -737,7 +795,7 @@ __global__ void __launch_bounds__(NT, 1) fps_grid_kernel(const BucketParams prm)
         }
       };
 #pragma unroll
-      for (int j = KM; j > 0; j >>= 1) stage(j);
+      for (int j = (KM < 32 ? KM : 16); j > 0; j >>= 1) stage(j);
       if constexpr (CL == 4) {
         // lanes 16..31 hold the second sorted 16-list: reverse it, merge 32
         const int src = lane < 2 * KM ? lane : 3 * 2 * KM - 1 - lane;

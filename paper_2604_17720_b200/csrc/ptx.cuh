@@ -103,4 +103,9 @@ __device__ __forceinline__ void st_async_b64(uint32_t raddr, uint32_t rbar, uint
                : "memory");
 }
 
+// start an L2 -> L1 fill of the 128-B line holding p (no register result)
+__device__ __forceinline__ void prefetch_l1(const void* p) {
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+}
+
 }  // namespace ffps

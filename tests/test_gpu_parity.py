@@ -25,15 +25,22 @@ class _Sched:
 
     def __enter__(self):
         from paper_2604_17720_b200 import _device
-        self.prev = _device.set_schedule(self.name)
+        name, _, km = self.name.partition("/km")  # "grid@2/km8": K1g with KM = 8
+        self.prev_km = os.environ.pop("FFPS_GRID_KM", None)
+        if km:
+            os.environ["FFPS_GRID_KM"] = km
+        self.prev = _device.set_schedule(name)
         return self
 
     def __exit__(self, *exc):
         from paper_2604_17720_b200 import _device
         _device.set_schedule(self.prev)
+        os.environ.pop("FFPS_GRID_KM", None)
+        if self.prev_km is not None:
+            os.environ["FFPS_GRID_KM"] = self.prev_km
 
 
-SCHEDULES = ["stream", "bucket", "multi", "grid", "grid@1", "grid@2"]
+SCHEDULES = ["stream", "bucket", "multi", "grid", "grid@1", "grid@2", "grid@2/km8"]
 
 
 @pytest.fixture(params=SCHEDULES)
@@ -280,7 +287,8 @@ def test_abi_rejects_bad_arguments(cuda):
     assert lib.ffps_fill_slice(0, 1, 1, 1, 10, 5, 4, None) == -1
 
 
-@pytest.mark.parametrize("sched", ["bucket", "multi", "grid@1", "grid@2", "grid@4"])
+@pytest.mark.parametrize("sched", ["bucket", "multi", "grid@1", "grid@2", "grid@4", "grid@1/km8",
+                                   "grid@2/km8"])
 @pytest.mark.parametrize("dtype", [np.float32, np.float64])
 def test_bucketed_schedule_sizes_and_ties(cuda, dtype, sched):
     """K0+K1b / K0+K1m / K1g forced on every size class: n below / at / above
@@ -297,7 +305,7 @@ def test_bucketed_schedule_sizes_and_ties(cuda, dtype, sched):
 
 
 @pytest.mark.parametrize("dtype", [np.float32, np.float64])
-@pytest.mark.parametrize("sched", ["multi", "grid@1", "grid@2", "grid@4"])
+@pytest.mark.parametrize("sched", ["multi", "grid@1", "grid@2", "grid@4", "grid@2/km8"])
 def test_multi_winner_degenerate_ties(cuda, dtype, sched):
     """K1m when hundreds of bucket keys tie (identical points, exhausted
     buckets): the candidate list overflows and rounds fall back to one exact
