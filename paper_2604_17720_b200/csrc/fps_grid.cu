@@ -540,6 +540,7 @@ __global__ void __launch_bounds__(NT, 1) fps_grid_kernel(const BucketParams prm)
     //    bucket per lane): top-2 keys by (value desc, position asc) + third value
     //    (only the groups with a re-evaluated bucket changed: the dirty list)
     if (tid < KM * NCG) compv_s[tid] = A::kmin;  // R1 fills the ranks it finds
+    if (tid < KM) topg_s[tid] = -1;              // ranks of empty groups stay -1
     for (int wd = 0, base = 0; wd < ((ng + 31) >> 5); ++wd) {
       const unsigned mword = dmask_s[wd];
       const int cw = __popc(mword);
@@ -595,7 +596,6 @@ __global__ void __launch_bounds__(NT, 1) fps_grid_kernel(const BucketParams prm)
 #pragma unroll
         for (int o = 1; o < 16; o <<= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
         if (part == 0 && v != A::kmin) {
-          atomicAdd(&ngv_s, 1);
           if (cnt < KM) {
             topg_s[cnt] = g;
 #pragma unroll
@@ -611,7 +611,7 @@ __global__ void __launch_bounds__(NT, 1) fps_grid_kernel(const BucketParams prm)
     __syncthreads();  // group ranks final
     // R2. all threads: ranks among the candidates of the top groups (<= KM * NCG
     //     <= 64, compacted by R1), 8 threads per candidate
-    const int ngt = ngv_s < KM ? ngv_s : KM;
+    const int ngt = __popc(__ballot_sync(0xffffffffu, lane < KM && topg_s[lane] >= 0));
     const int nrc = ngt * NCG;
     {
       constexpr int NC = KM * NCG;
