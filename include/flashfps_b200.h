@@ -83,15 +83,18 @@ int ffps_run_kernel(int dtype, const void* xyz, int64_t batch,
  *   FFPS_ALGO_MULTI   K0 + K1m: the bucketed schedule taking up to 8 consecutive
  *                     greedy winners per reduction round (the longest prefix of
  *                     the top candidates provably unaffected by each other);
- *   FFPS_ALGO_GRID    K0 + K1g: MULTI with the buckets indexed by a cell grid, so
+ *   FFPS_ALGO_GRID    K0 + K1g: up to 16 winners per round, the buckets held in
+ *                     shared memory and indexed by groups of 32 (kd order), so
  *                     a selected point only tests the buckets within its reach;
  *                     each cloud's buckets are split over a cluster of 1, 2 or
  *                     4 CTAs: FFPS_ALGO_GRID_CL(c) fixes c, plain FFPS_ALGO_GRID
- *                     picks the largest c with batch * c <= SM count;
- *   FFPS_ALGO_AUTO    GRID for n >= 65536 (any batch) or n >= 24576 with >= 16
- *                     clouds; BUCKET for mid-size clouds when the batch fills
- *                     the GPU; else STREAM (the environment variable
- *                     FFPS_ALGO=stream|bucket|multi|grid overrides AUTO). */
+ *                     takes 2 for n >= 20000 while batch * 2 <= SM count, else 1;
+ *   FFPS_ALGO_AUTO    GRID for n >= 16384 (any batch) or n >= 12288 with >= 16
+ *                     clouds, 2 CTAs per cloud from n >= 20000 while the
+ *                     batch fits the SMs twice; BUCKET for smaller clouds when
+ *                     the batch fills the GPU; else STREAM (the environment
+ *                     variable FFPS_ALGO=stream|bucket|multi|grid overrides
+ *                     AUTO). */
 enum ffps_algo { FFPS_ALGO_AUTO = 0, FFPS_ALGO_STREAM = 1, FFPS_ALGO_BUCKET = 2,
                  FFPS_ALGO_MULTI = 3, FFPS_ALGO_GRID = 4 };
 #define FFPS_ALGO_GRID_CL(c) (FFPS_ALGO_GRID | ((c) << 8))

@@ -600,20 +600,19 @@ int run_streaming(int dtype, const void* xyz, int64_t batch, int64_t cloud_strid
   return FFPS_OK;
 }
 
-// FFPS_ALGO_AUTO (measured on B200 over batch 1..128 x n 4K..128K with
-// iters = n/4, tools/sweep_auto.py, profiles/r01_sweep_auto.jsonl):
-//   GRID   (multi-winner rounds, cell index, 1-4 CTAs per cloud) for clouds of
-//          >= 64K points at any batch, and >= 24K points once >= 16 clouds;
-//   BUCKET (one CTA per cloud, exact bucket bounds) for mid-size clouds when the
-//          batch fills the GPU (>= 16 clouds of >= 12K points, >= 48 of >= 6K,
-//          >= 96 of >= 3K);
+// FFPS_ALGO_AUTO (measured on B200 over batch 1..128 x n 8K..200K with
+// iters = n/4, tools/sweep_cl.py --grid, profiles/r01_sweep_cl.jsonl; the time
+// per cloud is flat in the batch until the clusters outnumber the SMs):
+//   GRID   (multi-winner rounds, bucket-group index) for clouds of >= 16K
+//          points, and >= 12K points once >= 16 clouds;
+//   BUCKET (one CTA per cloud, exact bucket bounds) for smaller clouds when the
+//          batch fills the GPU (>= 48 clouds of >= 6K points, >= 96 of >= 3K);
 //   STREAM (clusters of up to 16 CTAs, every point every iteration) otherwise.
 // FFPS_ALGO in the environment ("stream" / "bucket" / "multi" / "grid")
 // overrides AUTO.
 int auto_algo(int64_t n, int64_t batch) {
-  if (n >= 65536 || (n >= 24576 && batch >= 16)) return FFPS_ALGO_GRID;
-  if ((n >= 12288 && batch >= 16) || (n >= 6144 && batch >= 48) || (n >= 3072 && batch >= 96))
-    return FFPS_ALGO_BUCKET;
+  if (n >= 16384 || (n >= 12288 && batch >= 16)) return FFPS_ALGO_GRID;
+  if ((n >= 6144 && batch >= 48) || (n >= 3072 && batch >= 96)) return FFPS_ALGO_BUCKET;
   return FFPS_ALGO_STREAM;
 }
 
@@ -632,16 +631,13 @@ int resolve_algo(int algo, int64_t n, int64_t batch) {
 }
 
 // CTAs per cloud of the grid schedule: fixed by the algo argument
-// (FFPS_ALGO_GRID_CL), else the largest of 1/2/4 with batch * c <= SMs;
-// FFPS_GRID_CL in the environment overrides both
+// (FFPS_ALGO_GRID_CL), else 2 for clouds of >= 20K points while batch * 2 <= SMs
+// (each CTA keeps >= 10 bucket groups for the KM = 16 candidates), else 1.
+// 4 CTAs per cloud (KM = 8) was never the fastest in the sweep (sweep_cl.py).
+// FFPS_GRID_CL in the environment overrides both.
 int grid_cluster(int algo, int64_t batch, int sms, int64_t n) {
   int cl = algo >> 8;
-  if (cl == 0) {
-    // spread the batch over the SMs, but keep >= 512 buckets of 32 points per
-    // CTA: fewer leave too few bucket groups to hold KM candidates
-    cl = 1;
-    while (cl < 4 && batch * (cl * 2) <= sms && (n + 31) / 32 >= 512 * (cl * 2)) cl *= 2;
-  }
+  if (cl == 0) cl = (n >= 20000 && batch * 2 <= sms) ? 2 : 1;
   if (const char* v = getenv("FFPS_GRID_CL")) {
     const int w = atoi(v);
     if (w == 1 || w == 2 || w == 4) cl = w;
