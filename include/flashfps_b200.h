@@ -126,6 +126,21 @@ int ffps_run_kernel_ex(int dtype, const void* xyz, int64_t batch,
 int ffps_fill_slice(int dtype, int64_t* order, void* sel_d2, int64_t batch,
                     int64_t out_stride, int64_t k, int64_t m1, void* stream);
 
+/* Budget fill, FillMode.SEEDED_RANDOM (fps_prune.py:96-103): for every cloud
+ * writes order[b][k + w], w < m1 - k, = the w-th entry of
+ *     np.random.default_rng(seed).choice(pool, m1 - k, replace=False)
+ * with pool the ascending complement of order[b][0:k) in [0, n), and
+ * sel_d2[b][k + w] = 0.  The generator state is NumPy's PCG64(seed) state
+ * (np.random.PCG64(seed).state: 128-bit state and increment, split in
+ * high/low 64-bit halves); every cloud starts from it, as the reference
+ * seeds one generator per call.  Draws follow NumPy 2.x's Generator.choice
+ * (tail partial Fisher-Yates or Floyd + shuffle, Lemire bounded integers),
+ * bit-identical to NumPy (oracle/npchoice.py pins the restatement). */
+int ffps_fill_random(int dtype, int64_t* order, void* sel_d2, int64_t batch,
+                     int64_t out_stride, int64_t n, int64_t k, int64_t m1,
+                     uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi,
+                     uint64_t inc_lo, void* stream);
+
 /* Covering radius of samples (replaces coverage_radius / _min_dist2_to,
  * metrics.py:29-52): out_d2[b] = max over p in xyz[b][0:n) of min over
  * i < m of d2(p, xyz[b][idx[b][i]]), the reference's rounded d2; the caller

@@ -129,6 +129,21 @@ def fill_slice(order: torch.Tensor, sel: torch.Tensor, k: int, m1: int, stream=N
                                   order.stride(0), k, m1, _stream_handle(stream)))
 
 
+def fill_random(order: torch.Tensor, sel: torch.Tensor, n: int, k: int, m1: int, rng_seed: int,
+                stream=None) -> None:
+    """K2r: order[:, k:m1] <- np.random.default_rng(rng_seed).choice(pool, m1 - k,
+    replace=False) of each cloud's unselected indices, sel[:, k:m1] <- 0.  Only
+    the generator's seeding (SeedSequence -> PCG64 state) runs on the host."""
+    B = order.shape[0]
+    if B == 0 or m1 <= k:
+        return
+    st = np.random.PCG64(rng_seed).state["state"]
+    with torch.cuda.device(order.device):
+        _count(_native.fill_random(dtype_code(sel), order.data_ptr(), sel.data_ptr(), B,
+                                   order.stride(0), n, k, m1,
+                                   (int(st["state"]), int(st["inc"])), _stream_handle(stream)))
+
+
 def seeds_tensor(seed_index, B: int, device) -> torch.Tensor:
     """(B,) int64 seed positions on ``device``, stream-ordered (no host sync
     when every cloud starts from the same position)."""

@@ -35,6 +35,8 @@ SIGNATURES = {
     "ffps_run_kernel_ex": (_int, [_int, _vp, _i64, _i64, _i64, _i64, _vp, _vp, _i64, _vp,
                                   _vp, _i64, _vp, _int]),
     "ffps_fill_slice": (_int, [_int, _vp, _vp, _i64, _i64, _i64, _i64, _vp]),
+    "ffps_fill_random": (_int, [_int, _vp, _vp, _i64, _i64, _i64, _i64, _i64, ctypes.c_uint64,
+                                ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64, _vp]),
     "ffps_coverage": (_int, [_int, _vp, _i64, _i64, _i64, _vp, _i64, _i64, _vp, _vp]),
     "ffps_plan": (_int, [_int, _i64, _i64, ctypes.POINTER(_i64)]),
     "ffps_bucket_plan": (_int, [_int, _i64, ctypes.POINTER(_i64)]),
@@ -88,6 +90,17 @@ def fill_slice(dtype, order, sel_d2, batch, out_stride, k, m1, stream) -> int:
     lib = load()
     check(lib.ffps_fill_slice(dtype, order, sel_d2, batch, out_stride, k, m1, stream),
           "ffps_fill_slice")
+    return int(lib.ffps_last_launch_count())
+
+
+def fill_random(dtype, order, sel_d2, batch, out_stride, n, k, m1, pcg_state, stream) -> int:
+    """pcg_state = (state, inc) of np.random.PCG64(seed) as Python ints."""
+    lib = load()
+    st, inc = pcg_state
+    m64 = (1 << 64) - 1
+    check(lib.ffps_fill_random(dtype, order, sel_d2, batch, out_stride, n, k, m1,
+                               (st >> 64) & m64, st & m64, (inc >> 64) & m64, inc & m64, stream),
+          "ffps_fill_random")
     return int(lib.ffps_last_launch_count())
 
 

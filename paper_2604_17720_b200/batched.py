@@ -125,21 +125,6 @@ def fps_batch(xyz, m: int, seed_index=0, *, device=None) -> tuple[BatchSample, S
             SamplerStats(distance_evals=n * (m - 1), iterations=m, candidates=n))
 
 
-def _random_fill(order: torch.Tensor, sel: torch.Tensor, k: int, m1: int, n: int,
-                 rng_seed: int) -> None:
-    """FillMode.SEEDED_RANDOM (fps_prune.py:101-103) — NumPy's Generator.choice
-    on the host, same call as the reference; off the default path."""
-    picks = order[:, :k].cpu().numpy()
-    fills = np.empty((picks.shape[0], m1 - k), dtype=np.int64)
-    for b in range(picks.shape[0]):
-        remaining = np.ones(n, dtype=bool)
-        remaining[picks[b]] = False
-        pool = np.flatnonzero(remaining)
-        fills[b] = np.random.default_rng(rng_seed).choice(pool, size=m1 - k, replace=False)
-    order[:, k:m1].copy_(torch.from_numpy(fills))
-    sel[:, k:m1].zero_()
-
-
 def _fps_prune_checks(B: int, n: int, m1: int, cfg: PruneConfig, seeds: np.ndarray):
     """fps_prune.py:78-88 — returns (k, c)."""
     if not 1 <= m1 <= n:
@@ -171,7 +156,7 @@ def _fps_prune_device(x: torch.Tensor, m1: int, cfg: PruneConfig, seeds: np.ndar
         if cfg.fill_mode is FillMode.DETERMINISTIC_SLICE:
             _device.fill_slice(order, sel, k, m1)
         else:
-            _random_fill(order, sel, k, m1, n, cfg.rng_seed)
+            _device.fill_random(order, sel, n, k, m1, cfg.rng_seed)
     return (BatchSample(order, sel, k),
             SamplerStats(distance_evals=c * (k - 1), iterations=k, candidates=c))
 

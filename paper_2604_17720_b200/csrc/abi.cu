@@ -851,4 +851,31 @@ int ffps_fill_slice(int dtype, int64_t* order, void* sel_d2, int64_t batch, int6
   return FFPS_OK;
 }
 
+int ffps_fill_random(int dtype, int64_t* order, void* sel_d2, int64_t batch, int64_t out_stride,
+                     int64_t n, int64_t k, int64_t m1, uint64_t state_hi, uint64_t state_lo,
+                     uint64_t inc_hi, uint64_t inc_lo, void* stream) {
+  g_last_launches = 0;
+  if (dtype != FFPS_F32 && dtype != FFPS_F64)
+    return fail(FFPS_EINVAL, "dtype must be FFPS_F32 or FFPS_F64");
+  if (batch < 0 || k < 1 || m1 < k || out_stride < m1 || n < m1)
+    return fail(FFPS_EINVAL, "fill: need 1 <= k <= m1 <= min(n, out_stride)");
+  if (n >= 0x7fffffffLL) return fail(FFPS_EUNSUPPORTED, "fill: n must be < 2^31");
+  if (batch == 0 || m1 == k) return FFPS_OK;
+  if (!order || !sel_d2) return fail(FFPS_EINVAL, "null device pointer");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int64_t words = ffps::fill_random_scratch_words(n, k, m1);
+  uint32_t* scratch = nullptr;
+  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&scratch),
+                                  (size_t)words * 4 * (size_t)batch, st);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync(fill_random)");
+  const uint64_t pcg[4] = {state_hi, state_lo, inc_hi, inc_lo};
+  e = ffps::launch_fill_random(dtype, order, sel_d2, batch, out_stride, n, k, m1, pcg, scratch,
+                               st);
+  cudaError_t e2 = cudaFreeAsync(scratch, st);
+  if (e != cudaSuccess) return cuda_fail(e, "fill_random_kernel launch");
+  if (e2 != cudaSuccess) return cuda_fail(e2, "cudaFreeAsync(fill_random)");
+  g_last_launches = 1;
+  return FFPS_OK;
+}
+
 }  // extern "C"

@@ -135,4 +135,10 @@ cudaError_t launch_coverage(int dtype, const CoverageParams& p, int64_t batch, i
 cudaError_t launch_fill_slice(int dtype, int64_t* order, void* sel_d2, int64_t batch,
                               int64_t out_stride, int64_t k, int64_t m1, cudaStream_t st);
 
+// K2r: seeded random fill (fill_random.cu); scratch = batch * words uint32.
+int64_t fill_random_scratch_words(int64_t n, int64_t k, int64_t m1);
+cudaError_t launch_fill_random(int dtype, int64_t* order, void* sel_d2, int64_t batch,
+                               int64_t out_stride, int64_t n, int64_t k, int64_t m1,
+                               const uint64_t pcg[4], uint32_t* scratch, cudaStream_t st);
+
 }  // namespace ffps

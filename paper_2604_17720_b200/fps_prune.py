@@ -6,9 +6,9 @@ slice (fps_prune.py:54-65), so on the device it is only the point count the
 greedy kernel is launched with; iteration pruning is the kernel's iteration
 count floor((1-p)M1) (fps_prune.py:45-47), both computed here in IEEE double
 exactly like the reference (e.g. p=0.9, M1=6000 gives 599, not 600).  The
-slice fill runs on the device (K2); the seeded random fill reproduces
-``numpy.random.default_rng(rng_seed).choice`` on the host — it is off the
-default path (FillMode.DETERMINISTIC_SLICE).
+slice fill (K2) and the seeded random fill (K2r, NumPy's
+``default_rng(rng_seed).choice(pool, fill_n, replace=False)`` restated on the
+device step for step, csrc/fill_random.cu) both run on the GPU.
 """
 
 from __future__ import annotations

@@ -316,3 +316,33 @@ def test_multi_winner_degenerate_ties(cuda, dtype, sched):
             pts = np.zeros((2, N, 3))
             pts[:, : N // 50] = rng.random((2, N // 50, 3))  # 2% distinct, 98% duplicates
             _check_batch(np.ascontiguousarray(pts.astype(dtype)), m, np.array([0, N - 1]))
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+@pytest.mark.parametrize("n,m1,p,rng_seed", [
+    (24000, 6000, 0.75, 0),      # tail partial Fisher-Yates (pop > 10000, fill > pop // 50)
+    (200000, 50000, 0.75, 3),    # C5 shape; seed 3 hits Lemire's rejection loop
+    (30000, 30000, 0.5, 5),      # tail with pop == fill (slot 0 keeps its value)
+    (5000, 2000, 0.5, 1),        # Floyd + shuffle (pop <= 10000)
+    (60000, 1100, 0.05, 2),      # Floyd with pop > 10000, fill <= pop // 50
+    (3000, 3000, 0.5, 7),        # Floyd with pop == fill
+])
+def test_seeded_random_fill_matches_numpy(cuda, n, m1, p, rng_seed, dtype):
+    """K2r: FillMode.SEEDED_RANDOM on the device equals
+    np.random.default_rng(rng_seed).choice(pool, m1 - k, replace=False) of the
+    reference (fps_prune.py:96-103) for every cloud, bit for bit."""
+    rng = np.random.default_rng(41)
+    B = 3
+    pts = rng.random((B, n, 3)).astype(dtype)
+    cfg = ffps.PruneConfig(p=p, fill_mode=ffps.FillMode.SEEDED_RANDOM, rng_seed=rng_seed)
+    out, _ = ffps.fps_prune_batch(torch.from_numpy(pts).cuda(), m1, cfg, seed_index=0)
+    k = out.fill_boundary
+    idx = out.indices.cpu().numpy()
+    sel = out.selection_dist2.cpu().numpy()
+    for b in range(B):
+        remaining = np.ones(n, dtype=bool)
+        remaining[idx[b, :k]] = False
+        want = np.random.default_rng(rng_seed).choice(np.flatnonzero(remaining), size=m1 - k,
+                                                      replace=False)
+        assert np.array_equal(idx[b, k:], want), (n, m1, p, b)
+        assert (sel[b, k:] == 0).all()
