@@ -17,6 +17,11 @@ from .errors import KernelError
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib",
                         "libflashfps_b200.so")
+# A/B builds of the same sources (tools/build_variant.sh) are loaded through
+# FFPS_LIB_VARIANT=<name> -> _lib/variants/libflashfps_b200_<name>.so
+if os.environ.get("FFPS_LIB_VARIANT"):
+    LIB_PATH = os.path.join(os.path.dirname(LIB_PATH), "variants",
+                            f"libflashfps_b200_{os.environ['FFPS_LIB_VARIANT']}.so")
 
 F32, F64 = 0, 1
 ALGO = {"auto": 0, "stream": 1, "bucket": 2, "multi": 3, "grid": 4,

@@ -378,7 +378,7 @@ int run_bucketed(int dtype, const void* xyz, int64_t batch, int64_t cloud_stride
     cudaFreeAsync(scratch, st);
     return cuda_fail(e, "fps_bucket_kernel launch");
   }
-  g_last_launches = 2;
+  g_last_launches = 1 + ffps::bucket_build_launches(bb);
   e = cudaFreeAsync(scratch, st);
   if (e != cudaSuccess) return cuda_fail(e, "cudaFreeAsync(buckets)");
   return FFPS_OK;
@@ -523,7 +523,7 @@ int run_grid(int dtype, const void* xyz, int64_t batch, int64_t cloud_stride, in
     cudaFreeAsync(scratch, st);
     return cuda_fail(e, "fps_grid_kernel launch");
   }
-  g_last_launches = 2;
+  g_last_launches = 1 + ffps::bucket_build_launches(bb);
   e = cudaFreeAsync(scratch, st);
   if (e != cudaSuccess) return cuda_fail(e, "cudaFreeAsync(grid)");
   return FFPS_OK;
@@ -801,11 +801,11 @@ int ffps_coverage(int dtype, const void* xyz, int64_t batch, int64_t cloud_strid
   int launches = 0;
   e = ffps::launch_bucket_build(dtype, bp, batch, st);
   if (e == cudaSuccess) {
-    ++launches;
+    launches += ffps::bucket_build_launches(bp);
     e = ffps::launch_bucket_build(dtype, bs, batch, st);
   }
   if (e == cudaSuccess) {
-    ++launches;
+    launches += ffps::bucket_build_launches(bs);
     e = cudaMemsetAsync(out_d2, 0, (size_t)batch * esz, st);
   }
   if (e == cudaSuccess) {

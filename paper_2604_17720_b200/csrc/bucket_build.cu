@@ -333,6 +333,11 @@ size_t bucket_build_smem() {
   return (size_t)(kCells + (kBuildThreads / 32) * kSub) * sizeof(uint32_t);
 }
 
+int bucket_build_launches(const BucketBuildParams& p) {
+  const char* kind = getenv("FFPS_BUCKET_BUILD");
+  return (p.TX != nullptr && !(kind && strcmp(kind, "morton") == 0)) ? 2 : 1;
+}
+
 cudaError_t launch_bucket_build(int dtype, const BucketBuildParams& p, int64_t batch,
                                 cudaStream_t st) {
   // default: kd-tree leaves (bucket_kd.cu; needs the TX..TO scratch);

@@ -30,6 +30,8 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
+#include <vector>
 
 #include "ffps_internal.h"
 
@@ -99,6 +101,11 @@ __device__ __forceinline__ int bin_of(T v, T lo, T inv) {
 // split of a segment: nl points (a multiple of bs) to the left child
 __device__ __forceinline__ int left_size(int m, int bs) { return ((m / bs + 1) / 2) * bs; }
 
+// histogram layout: bin b lives at word haddr(b) = (b % 32) * 32 + b / 32, so
+// the 32 bins a lane owns in find_split ([32 * lane, 32 * lane + 32)) are read
+// by the warp without bank conflicts (word j * 32 + lane)
+__device__ __forceinline__ int haddr(int b) { return ((b & 31) << 5) | (b >> 5); }
+
 // warp: locate the boundary bin of rank nl in a 1024-bin histogram h
 // (lane owns bins [32 * lane, 32 * lane + 32)); returns bin, count before it
 // and the bin's own count (uniform across the warp)
@@ -106,7 +113,7 @@ __device__ __forceinline__ void find_split(const uint32_t* h, int nl, int lane, 
                                            int& before, int& mid) {
   uint32_t loc = 0;
 #pragma unroll 8
-  for (int j = 0; j < 32; ++j) loc += h[lane * 32 + j];
+  for (int j = 0; j < 32; ++j) loc += h[(j << 5) | lane];
   uint32_t incl = loc;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
@@ -115,23 +122,26 @@ __device__ __forceinline__ void find_split(const uint32_t* h, int nl, int lane, 
   }
   const unsigned hit = __ballot_sync(0xffffffffu, incl >= (uint32_t)nl);
   const int L = __ffs(hit) - 1;  // nl <= m - 1 < total, so some lane hits
-  int b = 0, bef = 0, c = 0;
-  if (lane == L) {
-    uint32_t run = incl - loc;
-    for (int j = 0; j < 32; ++j) {
-      const uint32_t v = h[lane * 32 + j];
-      if (run + v >= (uint32_t)nl) {
-        b = lane * 32 + j;
-        bef = (int)run;
-        c = (int)v;
-        break;
-      }
-      run += v;
-    }
+  // lane j takes bin 32 L + j: scan those 32 counts across the warp
+  const uint32_t run0 = __shfl_sync(0xffffffffu, incl - loc, L);
+  const uint32_t v = h[(lane << 5) | L];
+  uint32_t iv = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t u = __shfl_up_sync(0xffffffffu, iv, o);
+    if (lane >= o) iv += u;
   }
-  bstar = __shfl_sync(0xffffffffu, b, L);
-  before = __shfl_sync(0xffffffffu, bef, L);
-  mid = __shfl_sync(0xffffffffu, c, L);
+  const int J = __ffs(__ballot_sync(0xffffffffu, run0 + iv >= (uint32_t)nl)) - 1;
+  bstar = 32 * L + J;
+  before = (int)(run0 + __shfl_sync(0xffffffffu, iv - v, J));
+  mid = (int)__shfl_sync(0xffffffffu, v, J);
+}
+
+// shared memory of one warp of the leaf kernel: histogram, DFS stack
+// (start, size, parity, box) and, when staged, two SoA buffers of cap points
+__host__ __device__ constexpr size_t kd_leaves_warp_bytes(int cap, int esz) {
+  return ((size_t)kBins * 4 + (size_t)kStack * 3 * 4 + (kStack & 1) * 4 + (size_t)kStack * 6 * esz +
+          (size_t)2 * cap * (3 * esz + 4) + 15) / 16 * 16;
 }
 
 template <typename T>
@@ -143,7 +153,9 @@ struct Bufs {
 }  // namespace
 
 template <typename T>
-__global__ void __launch_bounds__(kThreads, 1) bucket_kd_kernel(const BucketBuildParams p) {
+__global__ void __launch_bounds__(kThreads, 1) bucket_kd_kernel(const BucketBuildParams p,
+                                                                int32_t* seg_hdr, int32_t* seg_sm,
+                                                                T* seg_box) {
   using O = Ord<T>;
   using I = typename O::I;
   extern __shared__ __align__(16) uint32_t hist[];  // [kMaxSeg][kBins] / [kNW][kBins], stack boxes
@@ -154,9 +166,6 @@ __global__ void __launch_bounds__(kThreads, 1) bucket_kd_kernel(const BucketBuil
   __shared__ I s_box[kMaxSeg][6];       // boxes of the current segments
   __shared__ I s_cbox[2 * kMaxSeg][6];  // boxes of their children
   __shared__ int s_S;
-  // warp phase stack
-  __shared__ int w_start[kNW][kStack], w_m[kNW][kStack], w_par[kNW][kStack];
-  T(*w_box)[kStack][6] = reinterpret_cast<T(*)[kStack][6]>(hist + kMaxSeg * kBins);
 
   const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int n = (int)p.n;
@@ -245,7 +254,7 @@ __global__ void __launch_bounds__(kThreads, 1) bucket_kd_kernel(const BucketBuil
       const T lo = s_lo[s], inv = s_inv[s];
       const T* v = ax == 0 ? src.x : (ax == 1 ? src.y : src.z);
       uint32_t* h = hist + s * kBins;
-      for (int i = tid; i < m; i += kThreads) atomicAdd(&h[bin_of(v[st + i], lo, inv)], 1u);
+      for (int i = tid; i < m; i += kThreads) atomicAdd(&h[haddr(bin_of(v[st + i], lo, inv))], 1u);
     }
     __syncthreads();
     if (warp < S && s_m[warp] > bs) {
@@ -368,195 +377,337 @@ __global__ void __launch_bounds__(kThreads, 1) bucket_kd_kernel(const BucketBuil
     __syncthreads();
   }
 
-  // 2. warp phase: depth-first splits of each remaining segment
-  {
-    uint32_t* h = hist + warp * kBins;
-    const int S = s_S;
-    for (int s0 = warp; s0 < S; s0 += kNW) {
-      int top = 0;
-      if (lane == 0) {
-        w_start[warp][0] = s_start[s0];
-        w_m[warp][0] = s_m[s0];
-        w_par[warp][0] = par;
-#pragma unroll
-        for (int c = 0; c < 6; ++c) w_box[warp][0][c] = O::dec(s_box[s0][c]);
-      }
-      top = 1;
-      __syncwarp();
-      while (top > 0) {
-        --top;
-        const int st = w_start[warp][top], m = w_m[warp][top], pr = w_par[warp][top];
-        T bx[6];
-#pragma unroll
-        for (int c = 0; c < 6; ++c) bx[c] = w_box[warp][top][c];
-        __syncwarp();
-        const Bufs<T> src = buf(pr), dst = buf(pr ^ 1);
-        if (m <= bs) {  // leaf: must end in the output arrays
-          if (pr == 1)
-            for (int i = lane; i < m; i += 32) {
-              out.x[st + i] = src.x[st + i];
-              out.y[st + i] = src.y[st + i];
-              out.z[st + i] = src.z[st + i];
-              out.o[st + i] = src.o[st + i];
-            }
-          continue;
-        }
-        const T e0 = bx[3] - bx[0], e1 = bx[4] - bx[1], e2 = bx[5] - bx[2];
-        const int ax = e0 >= e1 ? (e0 >= e2 ? 0 : 2) : (e1 >= e2 ? 1 : 2);
-        const T ext = ax == 0 ? e0 : (ax == 1 ? e1 : e2);
-        const T lo = bx[ax];
-        const T inv = ext > (T)0 ? (T)kBins / ext : (T)0;
-        const int nl = left_size(m, bs);
-        const T* v = ax == 0 ? src.x : (ax == 1 ? src.y : src.z);
-#pragma unroll 8
-        for (int j = 0; j < 32; ++j) h[lane * 32 + j] = 0u;
-        __syncwarp();
-        for (int i = lane; i < m; i += 32) atomicAdd(&h[bin_of(v[st + i], lo, inv)], 1u);
-        __syncwarp();
-        int bstar, lt, midc;
-        find_split(h, nl, lane, bstar, lt, midc);
-        const int take = nl - lt;
-        int cl = 0, cm = 0, cr = 0;
-        T a[2][3], z[2][3];
-#pragma unroll
-        for (int k = 0; k < 2; ++k)
-#pragma unroll
-          for (int c = 0; c < 3; ++c) {
-            a[k][c] = pinf;
-            z[k][c] = -pinf;
-          }
-        for (int i0 = 0; i0 < m; i0 += 32) {
-          const int i = i0 + lane;
-          const bool live = i < m;
-          T p3[3] = {T(0), T(0), T(0)};
-          int32_t o = 0;
-          int cat = 3;
-          if (live) {
-            p3[0] = src.x[st + i];
-            p3[1] = src.y[st + i];
-            p3[2] = src.z[st + i];
-            o = src.o[st + i];
-            const int bn = bin_of(p3[ax], lo, inv);
-            cat = bn < bstar ? 0 : (bn == bstar ? 1 : 2);
-          }
-          const unsigned m0 = __ballot_sync(0xffffffffu, cat == 0);
-          const unsigned m1 = __ballot_sync(0xffffffffu, cat == 1);
-          const unsigned m2 = __ballot_sync(0xffffffffu, cat == 2);
-          const unsigned below = (1u << lane) - 1u;
-          int pos = 0;
-          if (cat == 0) {
-            pos = cl + __popc(m0 & below);
-          } else if (cat == 1) {
-            const int t = cm + __popc(m1 & below);
-            pos = t < take ? lt + t : nl + (t - take);
-          } else if (cat == 2) {
-            pos = nl + (midc - take) + cr + __popc(m2 & below);
-          }
-          cl += __popc(m0);
-          cm += __popc(m1);
-          cr += __popc(m2);
-          if (live) {
-            dst.x[st + pos] = p3[0];
-            dst.y[st + pos] = p3[1];
-            dst.z[st + pos] = p3[2];
-            dst.o[st + pos] = o;
-            const int k = pos < nl ? 0 : 1;
-#pragma unroll
-            for (int c = 0; c < 3; ++c) {
-              a[k][c] = p3[c] < a[k][c] ? p3[c] : a[k][c];
-              z[k][c] = p3[c] > z[k][c] ? p3[c] : z[k][c];
-            }
-          }
-        }
-#pragma unroll
-        for (int k = 0; k < 2; ++k)
-#pragma unroll
-          for (int c = 0; c < 3; ++c) {
-            a[k][c] = wmin(a[k][c]);
-            z[k][c] = wmax(z[k][c]);
-          }
-        // push right then left (left processed first; order is irrelevant)
-        if (top + 2 > kStack) __trap();  // depth <= log2(n / BS) + 1 < kStack
-        if (lane == 0) {
-          w_start[warp][top] = st + nl;
-          w_m[warp][top] = m - nl;
-          w_par[warp][top] = pr ^ 1;
-#pragma unroll
-          for (int c = 0; c < 3; ++c) {
-            w_box[warp][top][c] = a[1][c];
-            w_box[warp][top][3 + c] = z[1][c];
-          }
-          w_start[warp][top + 1] = st;
-          w_m[warp][top + 1] = nl;
-          w_par[warp][top + 1] = pr ^ 1;
-#pragma unroll
-          for (int c = 0; c < 3; ++c) {
-            w_box[warp][top + 1][c] = a[0][c];
-            w_box[warp][top + 1][3 + c] = z[0][c];
-          }
-        }
-        top += 2;
-        __syncwarp();
-      }
-    }
+  // 2. hand the segments to the leaf kernel: count, parity of the buffer that
+  //    holds them, (start, size) and box of each
+  if (tid == 0) {
+    seg_hdr[2 * b + 0] = s_S;
+    seg_hdr[2 * b + 1] = par;
   }
-  __syncthreads();
-
-  // 3. running distances, padding of the last bucket, bucket boxes
-  T* X = out.x;
-  T* Y = out.y;
-  T* Z = out.z;
-  int32_t* Ob = out.o;
-  for (int s = tid; s < n; s += kThreads) D[s] = pinf;
-  const int first_last = (int)((p.nbuckets - 1) * p.bs);
-  for (int s = n + tid; s < (int)p.nslots; s += kThreads) {
-    X[s] = X[first_last];
-    Y[s] = Y[first_last];
-    Z[s] = Z[first_last];
-    D[s] = -pinf;
-    Ob[s] = -1;
-  }
-  __syncthreads();
-  for (int q = warp; q < (int)p.nbuckets; q += kNW) {
-    T a[3] = {pinf, pinf, pinf}, z[3] = {-pinf, -pinf, -pinf};
-    for (int u = lane; u < bs; u += 32) {
-      const int s = q * bs + u;
-      const T v[3] = {X[s], Y[s], Z[s]};
+  if (tid < s_S) {
+    seg_sm[((int64_t)b * kMaxSeg + tid) * 2 + 0] = s_start[tid];
+    seg_sm[((int64_t)b * kMaxSeg + tid) * 2 + 1] = s_m[tid];
 #pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        a[c] = v[c] < a[c] ? v[c] : a[c];
-        z[c] = v[c] > z[c] ? v[c] : z[c];
-      }
-    }
-#pragma unroll
-    for (int c = 0; c < 3; ++c) {
-      a[c] = wmin(a[c]);
-      z[c] = wmax(z[c]);
-    }
-    if (lane == 0) {
-#pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        BB[(int64_t)q * 6 + c] = a[c];
-        BB[(int64_t)q * 6 + 3 + c] = z[c];
-      }
-    }
+    for (int c = 0; c < 6; ++c) seg_box[((int64_t)b * kMaxSeg + tid) * 6 + c] = O::dec(s_box[tid][c]);
   }
 }
 
-// histograms + the per-warp stack boxes (sized for double)
-size_t bucket_kd_smem() {
-  return (size_t)kMaxSeg * kBins * sizeof(uint32_t) + (size_t)kNW * kStack * 6 * sizeof(double);
+// K0-kd, second kernel: one warp per segment of the CTA phase, depth-first
+// splits down to the leaves (= buckets).  When the host's bound `cap` on the
+// segment size fits shared memory, the warp stages its segment there and
+// ping-pongs between two shared-memory buffers (every pass is then an LDS/STS
+// loop instead of an L2 round trip per 32 points); otherwise (cap == 0) it
+// works on the global arrays as the CTA phase does.  Each finished leaf is
+// written to the output arrays with its running distances (+inf), its box,
+// and — for the last bucket — the padding slots (first point of the bucket,
+// D = -inf, O = -1).
+template <typename T>
+__global__ void __launch_bounds__(128) bucket_kd_leaves_kernel(const BucketBuildParams p,
+                                                               const int32_t* seg_hdr,
+                                                               const int32_t* seg_sm,
+                                                               const T* seg_box, int cap,
+                                                               int wpc) {
+  extern __shared__ __align__(16) unsigned char kd_smem[];
+  const int b = blockIdx.y, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int s0 = blockIdx.x * wpc + warp;
+  const int S = seg_hdr[2 * b + 0], par0 = seg_hdr[2 * b + 1];
+  if (warp >= wpc || s0 >= S) return;  // warps are independent (no block barriers)
+  const int n = (int)p.n;
+  const int bs = (int)p.bs;
+  const int64_t base = (int64_t)b * p.nslots;
+  const Bufs<T> out{static_cast<T*>(p.X) + base, static_cast<T*>(p.Y) + base,
+                   static_cast<T*>(p.Z) + base, p.O + base};
+  const Bufs<T> tmp{static_cast<T*>(p.TX) + base, static_cast<T*>(p.TY) + base,
+                    static_cast<T*>(p.TZ) + base, p.TO + base};
+  T* D = static_cast<T*>(p.D) + base;
+  T* BB = static_cast<T*>(p.BB) + (int64_t)b * p.nbuckets * 6;
+  const T pinf = (T)INFINITY;
+
+  // per-warp shared memory: histogram, DFS stack, then (staged) buffers A, B
+  unsigned char* wb = kd_smem + (size_t)warp * kd_leaves_warp_bytes(cap, (int)sizeof(T));
+  uint32_t* h = reinterpret_cast<uint32_t*>(wb);
+  int* w_start = reinterpret_cast<int*>(h + kBins);
+  int* w_m = w_start + kStack;
+  int* w_par = w_m + kStack;
+  T* w_box = reinterpret_cast<T*>(w_par + kStack + (kStack & 1));  // [kStack][6], 8-B aligned
+
+  const int st0 = seg_sm[((int64_t)b * kMaxSeg + s0) * 2 + 0];
+  const int m0 = seg_sm[((int64_t)b * kMaxSeg + s0) * 2 + 1];
+  Bufs<T> P0, P1;
+  if (cap > 0) {
+    // stage the segment: P[k] points at buffer k minus st0, so global
+    // positions index it directly
+    T* A = w_box + kStack * 6;
+    const Bufs<T> src = par0 ? tmp : out;
+    Bufs<T> bufA{A, A + cap, A + 2 * cap, reinterpret_cast<int32_t*>(A + 3 * cap)};
+    Bufs<T> bufB{A + 3 * cap + cap * 4 / (int)sizeof(T), nullptr, nullptr, nullptr};
+    bufB.y = bufB.x + cap;
+    bufB.z = bufB.x + 2 * cap;
+    bufB.o = reinterpret_cast<int32_t*>(bufB.x + 3 * cap);
+    for (int i = lane; i < m0; i += 32) {
+      bufA.x[i] = src.x[st0 + i];
+      bufA.y[i] = src.y[st0 + i];
+      bufA.z[i] = src.z[st0 + i];
+      bufA.o[i] = src.o[st0 + i];
+    }
+    P0 = Bufs<T>{bufA.x - st0, bufA.y - st0, bufA.z - st0, bufA.o - st0};
+    P1 = Bufs<T>{bufB.x - st0, bufB.y - st0, bufB.z - st0, bufB.o - st0};
+  } else {
+    P0 = par0 ? tmp : out;
+    P1 = par0 ? out : tmp;
+  }
+  if (lane == 0) {
+    w_start[0] = st0;
+    w_m[0] = m0;
+    w_par[0] = 0;
+#pragma unroll
+    for (int c = 0; c < 6; ++c) w_box[c] = seg_box[((int64_t)b * kMaxSeg + s0) * 6 + c];
+  }
+  int top = 1;
+  __syncwarp();
+  while (top > 0) {
+    --top;
+    const int st = w_start[top], m = w_m[top], pr = w_par[top];
+    T bx[6];
+#pragma unroll
+    for (int c = 0; c < 6; ++c) bx[c] = w_box[top * 6 + c];
+    __syncwarp();
+    const Bufs<T> src = pr ? P1 : P0, dst = pr ? P0 : P1;
+    if (m <= bs) {
+      // leaf = bucket q: into the output arrays (unless it already is there),
+      // D = +inf, box; the last bucket also gets its padding slots
+      const bool copy = src.x + st != out.x + st;
+      T a[3] = {pinf, pinf, pinf}, z[3] = {-pinf, -pinf, -pinf};
+      T f0 = T(0), f1 = T(0), f2 = T(0);
+      for (int i = lane; i < m; i += 32) {
+        const T v0 = src.x[st + i], v1 = src.y[st + i], v2 = src.z[st + i];
+        if (copy) {
+          out.x[st + i] = v0;
+          out.y[st + i] = v1;
+          out.z[st + i] = v2;
+          out.o[st + i] = src.o[st + i];
+        }
+        D[st + i] = pinf;
+        if (i == 0) {
+          f0 = v0;
+          f1 = v1;
+          f2 = v2;
+        }
+        a[0] = v0 < a[0] ? v0 : a[0];
+        a[1] = v1 < a[1] ? v1 : a[1];
+        a[2] = v2 < a[2] ? v2 : a[2];
+        z[0] = v0 > z[0] ? v0 : z[0];
+        z[1] = v1 > z[1] ? v1 : z[1];
+        z[2] = v2 > z[2] ? v2 : z[2];
+      }
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        a[c] = wmin(a[c]);
+        z[c] = wmax(z[c]);
+      }
+      const int q = st / bs;
+      if (lane == 0) {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          BB[(int64_t)q * 6 + c] = a[c];
+          BB[(int64_t)q * 6 + 3 + c] = z[c];
+        }
+      }
+      if (st + m == n && (int64_t)n < p.nslots) {
+        f0 = __shfl_sync(0xffffffffu, f0, 0);
+        f1 = __shfl_sync(0xffffffffu, f1, 0);
+        f2 = __shfl_sync(0xffffffffu, f2, 0);
+        for (int s = n + lane; s < (int)p.nslots; s += 32) {
+          out.x[s] = f0;
+          out.y[s] = f1;
+          out.z[s] = f2;
+          D[s] = -pinf;
+          out.o[s] = -1;
+        }
+      }
+      continue;
+    }
+    const T e0 = bx[3] - bx[0], e1 = bx[4] - bx[1], e2 = bx[5] - bx[2];
+    const int ax = e0 >= e1 ? (e0 >= e2 ? 0 : 2) : (e1 >= e2 ? 1 : 2);
+    const T ext = ax == 0 ? e0 : (ax == 1 ? e1 : e2);
+    const T lo = ax == 0 ? bx[0] : (ax == 1 ? bx[1] : bx[2]);
+    const T inv = ext > (T)0 ? (T)kBins / ext : (T)0;
+    const int nl = left_size(m, bs);
+    const T* v = ax == 0 ? src.x : (ax == 1 ? src.y : src.z);
+#pragma unroll 8
+    for (int j = 0; j < 32; ++j) h[(j << 5) | lane] = 0u;
+    __syncwarp();
+    for (int i = lane; i < m; i += 32) atomicAdd(&h[haddr(bin_of(v[st + i], lo, inv))], 1u);
+    __syncwarp();
+    int bstar, lt, midc;
+    find_split(h, nl, lane, bstar, lt, midc);
+    const int take = nl - lt;
+    int cl = 0, cm = 0, cr = 0;
+    T a[2][3], z[2][3];
+#pragma unroll
+    for (int k = 0; k < 2; ++k)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        a[k][c] = pinf;
+        z[k][c] = -pinf;
+      }
+    for (int i0 = 0; i0 < m; i0 += 32) {
+      const int i = i0 + lane;
+      const bool live = i < m;
+      T p3[3] = {T(0), T(0), T(0)};
+      int32_t o = 0;
+      int cat = 3;
+      if (live) {
+        p3[0] = src.x[st + i];
+        p3[1] = src.y[st + i];
+        p3[2] = src.z[st + i];
+        o = src.o[st + i];
+        const int bn = bin_of(ax == 0 ? p3[0] : (ax == 1 ? p3[1] : p3[2]), lo, inv);
+        cat = bn < bstar ? 0 : (bn == bstar ? 1 : 2);
+      }
+      const unsigned mk0 = __ballot_sync(0xffffffffu, cat == 0);
+      const unsigned mk1 = __ballot_sync(0xffffffffu, cat == 1);
+      const unsigned mk2 = __ballot_sync(0xffffffffu, cat == 2);
+      const unsigned below = (1u << lane) - 1u;
+      int pos = 0;
+      if (cat == 0) {
+        pos = cl + __popc(mk0 & below);
+      } else if (cat == 1) {
+        const int t = cm + __popc(mk1 & below);
+        pos = t < take ? lt + t : nl + (t - take);
+      } else if (cat == 2) {
+        pos = nl + (midc - take) + cr + __popc(mk2 & below);
+      }
+      cl += __popc(mk0);
+      cm += __popc(mk1);
+      cr += __popc(mk2);
+      if (live) {
+        dst.x[st + pos] = p3[0];
+        dst.y[st + pos] = p3[1];
+        dst.z[st + pos] = p3[2];
+        dst.o[st + pos] = o;
+        const bool left = pos < nl;  // registers only (no dynamic index)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          const T al = p3[c] < a[0][c] ? p3[c] : a[0][c], ar = p3[c] < a[1][c] ? p3[c] : a[1][c];
+          const T zl = p3[c] > z[0][c] ? p3[c] : z[0][c], zr = p3[c] > z[1][c] ? p3[c] : z[1][c];
+          a[0][c] = left ? al : a[0][c];
+          z[0][c] = left ? zl : z[0][c];
+          a[1][c] = left ? a[1][c] : ar;
+          z[1][c] = left ? z[1][c] : zr;
+        }
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < 2; ++k)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        a[k][c] = wmin(a[k][c]);
+        z[k][c] = wmax(z[k][c]);
+      }
+    if (top + 2 > kStack) __trap();  // depth <= log2(n / BS) + 1 < kStack
+    if (lane == 0) {  // push right then left (left processed first; order is irrelevant)
+      w_start[top] = st + nl;
+      w_m[top] = m - nl;
+      w_par[top] = pr ^ 1;
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        w_box[top * 6 + c] = a[1][c];
+        w_box[top * 6 + 3 + c] = z[1][c];
+      }
+      w_start[top + 1] = st;
+      w_m[top + 1] = nl;
+      w_par[top + 1] = pr ^ 1;
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        w_box[(top + 1) * 6 + c] = a[0][c];
+        w_box[(top + 1) * 6 + 3 + c] = z[0][c];
+      }
+    }
+    top += 2;
+    __syncwarp();
+  }
+}
+
+// histograms of the CTA phase
+size_t bucket_kd_smem() { return (size_t)kMaxSeg * kBins * sizeof(uint32_t); }
+
+// largest segment the CTA phase hands over: the split sizes depend on n and
+// the bucket size only (left_size), so the host replays the level loop
+static int kd_max_segment(int64_t n, int64_t bs) {
+  std::vector<int64_t> seg{n};
+  for (;;) {
+    bool any = false;
+    for (int64_t m : seg) any |= m > bs;
+    if (!any || 2 * seg.size() > (size_t)kMaxSeg) break;
+    std::vector<int64_t> nx;
+    for (int64_t m : seg) {
+      if (m > bs) {
+        const int64_t nl = ((m / bs + 1) / 2) * bs;
+        nx.push_back(nl);
+        nx.push_back(m - nl);
+      } else {
+        nx.push_back(m);
+      }
+    }
+    seg.swap(nx);
+  }
+  int64_t mx = 0;
+  for (int64_t m : seg) mx = m > mx ? m : mx;
+  return (int)mx;
 }
 
 cudaError_t launch_bucket_kd(int dtype, const BucketBuildParams& p, int64_t batch,
                              cudaStream_t st) {
-  const void* fn = dtype == 0 ? reinterpret_cast<const void*>(&bucket_kd_kernel<float>)
-                              : reinterpret_cast<const void*>(&bucket_kd_kernel<double>);
-  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)bucket_kd_smem());
+  const int esz = dtype == 0 ? 4 : 8;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
-  void* args[] = {const_cast<BucketBuildParams*>(&p)};
-  return cudaLaunchKernel(fn, dim3((unsigned)batch), dim3(kThreads), args, bucket_kd_smem(), st);
+  int optin = 0;
+  e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  if (e != cudaSuccess) return e;
+  // leaf kernel: up to 4 warps (segments) per CTA with their segments staged
+  // in shared memory; 2 or 1 for bigger segments; global arrays beyond that
+  const int mmax = kd_max_segment(p.n, p.bs);
+  int cap = (mmax + 31) / 32 * 32, wpc = 4;
+  while (wpc > 1 && (size_t)wpc * kd_leaves_warp_bytes(cap, esz) > (size_t)optin) wpc >>= 1;
+  if ((size_t)wpc * kd_leaves_warp_bytes(cap, esz) > (size_t)optin) {
+    cap = 0;
+    wpc = 4;
+  }
+  if (const char* v = getenv("FFPS_KD_STAGE"))  // A/B: 0 = leaves on the global arrays
+    if (atoi(v) == 0) {
+      cap = 0;
+      wpc = 4;
+    }
+  const size_t leaves_smem = (size_t)wpc * kd_leaves_warp_bytes(cap, esz);
+  // segment hand-off: [batch][2] header, [batch][kMaxSeg][2] (start, size),
+  // [batch][kMaxSeg][6] boxes
+  const size_t hdr_b = (size_t)batch * 2 * 4, sm_b = (size_t)batch * kMaxSeg * 2 * 4;
+  const size_t box_b = (size_t)batch * kMaxSeg * 6 * esz;
+  unsigned char* segs = nullptr;
+  e = cudaMallocAsync(reinterpret_cast<void**>(&segs), hdr_b + sm_b + box_b + 64, st);
+  if (e != cudaSuccess) return e;
+  int32_t* seg_hdr = reinterpret_cast<int32_t*>(segs);
+  int32_t* seg_sm = reinterpret_cast<int32_t*>(segs + hdr_b);
+  void* seg_box = segs + ((hdr_b + sm_b + 15) / 16) * 16;
+  const void* f1 = dtype == 0 ? reinterpret_cast<const void*>(&bucket_kd_kernel<float>)
+                              : reinterpret_cast<const void*>(&bucket_kd_kernel<double>);
+  const void* f2 = dtype == 0 ? reinterpret_cast<const void*>(&bucket_kd_leaves_kernel<float>)
+                              : reinterpret_cast<const void*>(&bucket_kd_leaves_kernel<double>);
+  e = cudaFuncSetAttribute(f1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bucket_kd_smem());
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(f2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)leaves_smem);
+  if (e == cudaSuccess) {
+    void* a1[] = {const_cast<BucketBuildParams*>(&p), &seg_hdr, &seg_sm, &seg_box};
+    e = cudaLaunchKernel(f1, dim3((unsigned)batch), dim3(kThreads), a1, bucket_kd_smem(), st);
+  }
+  if (e == cudaSuccess) {
+    void* a2[] = {const_cast<BucketBuildParams*>(&p), &seg_hdr, &seg_sm, &seg_box, &cap, &wpc};
+    e = cudaLaunchKernel(f2, dim3((unsigned)((kMaxSeg + wpc - 1) / wpc), (unsigned)batch),
+                         dim3(32 * wpc), a2, leaves_smem, st);
+  }
+  cudaError_t e2 = cudaFreeAsync(segs, st);
+  return e != cudaSuccess ? e : e2;
 }
 
 }  // namespace ffps

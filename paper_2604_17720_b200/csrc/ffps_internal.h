@@ -115,6 +115,8 @@ const GridInst* grid_instances(int* count);
 size_t grid_smem(int dtype, int64_t nb);
 size_t bucket_build_smem();
 size_t bucket_kd_smem();
+// kernel launches one launch_bucket_build issues (kd: CTA phase + leaf kernel)
+int bucket_build_launches(const BucketBuildParams& p);
 cudaError_t launch_bucket_kd(int dtype, const BucketBuildParams& p, int64_t batch,
                              cudaStream_t st);
 cudaError_t launch_bucket_build(int dtype, const BucketBuildParams& p, int64_t batch,

@@ -193,7 +193,11 @@ __global__ void __launch_bounds__(NT, 1) fps_grid_kernel(const BucketParams prm)
   bits_t* k2 = kv + nb;                                  // [nb] second-best value
   // per group (phase C): max key, the (NCG+1)-th value; candidates NCG*g + k =
   // the group's k-th best key (value, position, table row)
-  constexpr int NCG = KM <= 16 ? KM / 4 : 4;  // candidates per group
+#ifndef FFPS_GRID_NCG16
+#define FFPS_GRID_NCG16 4
+#endif
+  // candidates per group (A/B: FFPS_GRID_NCG16 for KM = 16)
+  constexpr int NCG = KM == 16 ? FFPS_GRID_NCG16 : (KM < 16 ? KM / 4 : 4);
   bits_t* gmax = k2 + nb;                                // [ng] group max key
   bits_t* gnext = gmax + ng;                             // [ng]
   bits_t* cand_v = gnext + ng;                           // [NCG ng]
