@@ -41,9 +41,11 @@ namespace {
 
 constexpr int kThreads = 1024;
 constexpr int kNW = kThreads / 32;
-constexpr int kBins = 1024;
-constexpr int kMaxSeg = kNW;   // CTA phase stops at this many segments
-constexpr int kStack = 24;     // per-warp DFS stack (depth <= log2(n / BS) + 1)
+constexpr int kBins1 = 512;    // CTA phase: bins per segment histogram
+constexpr int kBinsL = 256;    // leaf kernel: bins per warp histogram
+constexpr int kMaxSeg = 64;    // CTA phase stops at this many segments
+constexpr int kStack = 24;
+constexpr int kU = 4;          // CTA phase: points per thread in flight     // per-warp DFS stack (depth <= log2(n / BS) + 1)
 
 // order-preserving integer image of a float / double (for shared atomics)
 template <typename T>
@@ -92,28 +94,35 @@ __device__ __forceinline__ T wmax(T v) {
   return v;
 }
 
-template <typename T>
+template <int NB, typename T>
 __device__ __forceinline__ int bin_of(T v, T lo, T inv) {
   const int c = (int)((v - lo) * inv);
-  return c < 0 ? 0 : (c >= kBins ? kBins - 1 : c);
+  return c < 0 ? 0 : (c >= NB ? NB - 1 : c);
 }
 
 // split of a segment: nl points (a multiple of bs) to the left child
 __device__ __forceinline__ int left_size(int m, int bs) { return ((m / bs + 1) / 2) * bs; }
 
-// histogram layout: bin b lives at word haddr(b) = (b % 32) * 32 + b / 32, so
-// the 32 bins a lane owns in find_split ([32 * lane, 32 * lane + 32)) are read
-// by the warp without bank conflicts (word j * 32 + lane)
-__device__ __forceinline__ int haddr(int b) { return ((b & 31) << 5) | (b >> 5); }
+// histogram layout (NB bins, BPL = NB / 32 per lane): bin b lives at word
+// haddr(b) = (b % BPL) * 32 + b / BPL, so the BPL bins a lane owns in
+// find_split ([BPL * lane, BPL * lane + BPL)) are read by the warp without
+// bank conflicts (word j * 32 + lane)
+template <int NB>
+__device__ __forceinline__ int haddr(int b) {
+  constexpr int BPL = NB / 32;
+  return (b % BPL) * 32 + b / BPL;
+}
 
-// warp: locate the boundary bin of rank nl in a 1024-bin histogram h
-// (lane owns bins [32 * lane, 32 * lane + 32)); returns bin, count before it
-// and the bin's own count (uniform across the warp)
+// warp: locate the boundary bin of rank nl in an NB-bin histogram h; returns
+// bin, count before it and the bin's own count (uniform across the warp)
+template <int NB>
 __device__ __forceinline__ void find_split(const uint32_t* h, int nl, int lane, int& bstar,
                                            int& before, int& mid) {
+  constexpr int BPL = NB / 32;
+  static_assert(BPL >= 1 && BPL <= 32, "32 to 1024 bins");
   uint32_t loc = 0;
 #pragma unroll 8
-  for (int j = 0; j < 32; ++j) loc += h[(j << 5) | lane];
+  for (int j = 0; j < BPL; ++j) loc += h[j * 32 + lane];
   uint32_t incl = loc;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
@@ -122,17 +131,17 @@ __device__ __forceinline__ void find_split(const uint32_t* h, int nl, int lane, 
   }
   const unsigned hit = __ballot_sync(0xffffffffu, incl >= (uint32_t)nl);
   const int L = __ffs(hit) - 1;  // nl <= m - 1 < total, so some lane hits
-  // lane j takes bin 32 L + j: scan those 32 counts across the warp
+  // lane j < BPL takes bin BPL * L + j: scan those counts across the warp
   const uint32_t run0 = __shfl_sync(0xffffffffu, incl - loc, L);
-  const uint32_t v = h[(lane << 5) | L];
+  const uint32_t v = lane < BPL ? h[lane * 32 + L] : 0u;
   uint32_t iv = v;
 #pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
+  for (int o = 1; o < BPL; o <<= 1) {
     const uint32_t u = __shfl_up_sync(0xffffffffu, iv, o);
     if (lane >= o) iv += u;
   }
-  const int J = __ffs(__ballot_sync(0xffffffffu, run0 + iv >= (uint32_t)nl)) - 1;
-  bstar = 32 * L + J;
+  const int J = __ffs(__ballot_sync(0xffffffffu, lane < BPL && run0 + iv >= (uint32_t)nl)) - 1;
+  bstar = BPL * L + J;
   before = (int)(run0 + __shfl_sync(0xffffffffu, iv - v, J));
   mid = (int)__shfl_sync(0xffffffffu, v, J);
 }
@@ -140,7 +149,7 @@ __device__ __forceinline__ void find_split(const uint32_t* h, int nl, int lane, 
 // shared memory of one warp of the leaf kernel: histogram, DFS stack
 // (start, size, parity, box) and, when staged, two SoA buffers of cap points
 __host__ __device__ constexpr size_t kd_leaves_warp_bytes(int cap, int esz) {
-  return ((size_t)kBins * 4 + (size_t)kStack * 3 * 4 + (kStack & 1) * 4 + (size_t)kStack * 6 * esz +
+  return ((size_t)kBinsL * 4 + (size_t)kStack * 3 * 4 + (kStack & 1) * 4 + (size_t)kStack * 6 * esz +
           (size_t)2 * cap * (3 * esz + 4) + 15) / 16 * 16;
 }
 
@@ -187,17 +196,32 @@ __global__ void __launch_bounds__(kThreads, 1) bucket_kd_kernel(const BucketBuil
   __syncthreads();
   {
     T a[3] = {pinf, pinf, pinf}, z[3] = {-pinf, -pinf, -pinf};
-    for (int i = tid; i < n; i += kThreads) {
-      const int64_t s = map ? __ldg(map + i) : i;
-      const T v[3] = {X0[3 * s + 0], X0[3 * s + 1], X0[3 * s + 2]};
-      out.x[i] = v[0];
-      out.y[i] = v[1];
-      out.z[i] = v[2];
-      out.o[i] = i;
+    for (int i0 = 0; i0 < n; i0 += kThreads * kU) {  // kU points per thread in flight
+      T v[kU][3];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int i = i0 + u * kThreads + tid;
+        const int64_t s = i < n ? (map ? __ldg(map + i) : i) : 0;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) v[u][c] = i < n ? X0[3 * s + c] : T(0);
+      }
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int i = i0 + u * kThreads + tid;
+        if (i < n) {
+          out.x[i] = v[u][0];
+          out.y[i] = v[u][1];
+          out.z[i] = v[u][2];
+          out.o[i] = i;
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kU; ++u)
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
-        a[c] = v[c] < a[c] ? v[c] : a[c];
-        z[c] = v[c] > z[c] ? v[c] : z[c];
+        const bool in = i0 + u * kThreads + tid < n;
+        a[c] = in && v[u][c] < a[c] ? v[u][c] : a[c];
+        z[c] = in && v[u][c] > z[c] ? v[u][c] : z[c];
       }
     }
 #pragma unroll
@@ -237,7 +261,7 @@ __global__ void __launch_bounds__(kThreads, 1) bucket_kd_kernel(const BucketBuil
       const int ax = ext[0] >= ext[1] ? (ext[0] >= ext[2] ? 0 : 2) : (ext[1] >= ext[2] ? 1 : 2);
       s_ax[s] = ax;
       s_lo[s] = O::dec(s_box[s][ax]);
-      s_inv[s] = ext[ax] > (T)0 ? (T)kBins / ext[ax] : (T)0;
+      s_inv[s] = ext[ax] > (T)0 ? (T)kBins1 / ext[ax] : (T)0;
       s_nl[s] = s_m[s] > bs ? left_size(s_m[s], bs) : s_m[s];
       s_cl[s] = s_cm[s] = s_cr[s] = 0;
     }
@@ -245,7 +269,7 @@ __global__ void __launch_bounds__(kThreads, 1) bucket_kd_kernel(const BucketBuil
       const int c = tid % 6;
       s_cbox[tid / 6][c] = c < 3 ? O::kMax : O::kMin;
     }
-    for (int i = tid; i < S * kBins; i += kThreads) hist[i] = 0u;
+    for (int i = tid; i < S * kBins1; i += kThreads) hist[i] = 0u;
     __syncthreads();
     // histogram pass (segment-major: the whole CTA on one segment at a time)
     for (int s = 0; s < S; ++s) {
@@ -253,18 +277,29 @@ __global__ void __launch_bounds__(kThreads, 1) bucket_kd_kernel(const BucketBuil
       const int st = s_start[s], m = s_m[s], ax = s_ax[s];
       const T lo = s_lo[s], inv = s_inv[s];
       const T* v = ax == 0 ? src.x : (ax == 1 ? src.y : src.z);
-      uint32_t* h = hist + s * kBins;
-      for (int i = tid; i < m; i += kThreads) atomicAdd(&h[haddr(bin_of(v[st + i], lo, inv))], 1u);
+      uint32_t* h = hist + s * kBins1;
+      for (int i0 = 0; i0 < m; i0 += kThreads * kU) {  // kU loads in flight, then the atomics
+        T w[kU];
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+          const int i = i0 + u * kThreads + tid;
+          w[u] = i < m ? v[st + i] : T(0);
+        }
+#pragma unroll
+        for (int u = 0; u < kU; ++u)
+          if (i0 + u * kThreads + tid < m) atomicAdd(&h[haddr<kBins1>(bin_of<kBins1>(w[u], lo, inv))], 1u);
+      }
     }
     __syncthreads();
-    if (warp < S && s_m[warp] > bs) {
+    for (int sw = warp; sw < S; sw += kNW) {
+      if (s_m[sw] <= bs) continue;
       int bstar, before, mid;
-      find_split(hist + warp * kBins, s_nl[warp], lane, bstar, before, mid);
+      find_split<kBins1>(hist + sw * kBins1, s_nl[sw], lane, bstar, before, mid);
       if (lane == 0) {
-        s_b[warp] = bstar;
-        s_lt[warp] = before;
-        s_mid[warp] = mid;
-        s_take[warp] = s_nl[warp] - before;
+        s_b[sw] = bstar;
+        s_lt[sw] = before;
+        s_mid[sw] = mid;
+        s_take[sw] = s_nl[sw] - before;
       }
     }
     __syncthreads();
@@ -284,19 +319,28 @@ __global__ void __launch_bounds__(kThreads, 1) bucket_kd_kernel(const BucketBuil
           a[k][c] = pinf;
           z[k][c] = -pinf;
         }
-      for (int i0 = 0; i0 < m; i0 += kThreads) {  // warp-uniform trip count
-        const int i = i0 + tid;
+      for (int j0 = 0; j0 < m; j0 += kThreads * kU) {  // warp-uniform trip count
+       T vv[kU][3];
+       int32_t oo[kU];
+#pragma unroll
+       for (int u = 0; u < kU; ++u) {  // kU points per thread in flight
+         const int i = j0 + u * kThreads + tid;
+         const bool live = i < m;
+         vv[u][0] = live ? src.x[st + i] : T(0);
+         vv[u][1] = live ? src.y[st + i] : T(0);
+         vv[u][2] = live ? src.z[st + i] : T(0);
+         oo[u] = live ? src.o[st + i] : 0;
+       }
+#pragma unroll
+       for (int u = 0; u < kU; ++u) {
+        const int i = j0 + u * kThreads + tid;
         const bool live = i < m;
-        T v[3] = {T(0), T(0), T(0)};
-        int32_t o = 0;
+        const T v[3] = {vv[u][0], vv[u][1], vv[u][2]};
+        const int32_t o = oo[u];
         int cat = 3;  // 0 left, 1 boundary bin, 2 right
         if (live) {
-          v[0] = src.x[st + i];
-          v[1] = src.y[st + i];
-          v[2] = src.z[st + i];
-          o = src.o[st + i];
           if (split) {
-            const int bn = bin_of(v[ax], lo, inv);
+            const int bn = bin_of<kBins1>(ax == 0 ? v[0] : (ax == 1 ? v[1] : v[2]), lo, inv);
             cat = bn < bstar ? 0 : (bn == bstar ? 1 : 2);
           } else {
             cat = 0;
@@ -327,13 +371,18 @@ __global__ void __launch_bounds__(kThreads, 1) bucket_kd_kernel(const BucketBuil
           dst.y[st + pos] = v[1];
           dst.z[st + pos] = v[2];
           dst.o[st + pos] = o;
-          const int k = pos < nl ? 0 : 1;
+          const bool left = pos < nl;  // registers only (no dynamic index)
 #pragma unroll
           for (int c = 0; c < 3; ++c) {
-            a[k][c] = v[c] < a[k][c] ? v[c] : a[k][c];
-            z[k][c] = v[c] > z[k][c] ? v[c] : z[k][c];
+            const T al = v[c] < a[0][c] ? v[c] : a[0][c], ar = v[c] < a[1][c] ? v[c] : a[1][c];
+            const T zl = v[c] > z[0][c] ? v[c] : z[0][c], zr = v[c] > z[1][c] ? v[c] : z[1][c];
+            a[0][c] = left ? al : a[0][c];
+            z[0][c] = left ? zl : z[0][c];
+            a[1][c] = left ? a[1][c] : ar;
+            z[1][c] = left ? z[1][c] : zr;
           }
         }
+       }
       }
 #pragma unroll
       for (int k = 0; k < 2; ++k)
@@ -401,7 +450,7 @@ __global__ void __launch_bounds__(kThreads, 1) bucket_kd_kernel(const BucketBuil
 // and — for the last bucket — the padding slots (first point of the bucket,
 // D = -inf, O = -1).
 template <typename T>
-__global__ void __launch_bounds__(128) bucket_kd_leaves_kernel(const BucketBuildParams p,
+__global__ void __launch_bounds__(256) bucket_kd_leaves_kernel(const BucketBuildParams p,
                                                                const int32_t* seg_hdr,
                                                                const int32_t* seg_sm,
                                                                const T* seg_box, int cap,
@@ -425,7 +474,7 @@ __global__ void __launch_bounds__(128) bucket_kd_leaves_kernel(const BucketBuild
   // per-warp shared memory: histogram, DFS stack, then (staged) buffers A, B
   unsigned char* wb = kd_smem + (size_t)warp * kd_leaves_warp_bytes(cap, (int)sizeof(T));
   uint32_t* h = reinterpret_cast<uint32_t*>(wb);
-  int* w_start = reinterpret_cast<int*>(h + kBins);
+  int* w_start = reinterpret_cast<int*>(h + kBinsL);
   int* w_m = w_start + kStack;
   int* w_par = w_m + kStack;
   T* w_box = reinterpret_cast<T*>(w_par + kStack + (kStack & 1));  // [kStack][6], 8-B aligned
@@ -530,16 +579,16 @@ __global__ void __launch_bounds__(128) bucket_kd_leaves_kernel(const BucketBuild
     const int ax = e0 >= e1 ? (e0 >= e2 ? 0 : 2) : (e1 >= e2 ? 1 : 2);
     const T ext = ax == 0 ? e0 : (ax == 1 ? e1 : e2);
     const T lo = ax == 0 ? bx[0] : (ax == 1 ? bx[1] : bx[2]);
-    const T inv = ext > (T)0 ? (T)kBins / ext : (T)0;
+    const T inv = ext > (T)0 ? (T)kBinsL / ext : (T)0;
     const int nl = left_size(m, bs);
     const T* v = ax == 0 ? src.x : (ax == 1 ? src.y : src.z);
 #pragma unroll 8
-    for (int j = 0; j < 32; ++j) h[(j << 5) | lane] = 0u;
+    for (int j = 0; j < kBinsL / 32; ++j) h[j * 32 + lane] = 0u;
     __syncwarp();
-    for (int i = lane; i < m; i += 32) atomicAdd(&h[haddr(bin_of(v[st + i], lo, inv))], 1u);
+    for (int i = lane; i < m; i += 32) atomicAdd(&h[haddr<kBinsL>(bin_of<kBinsL>(v[st + i], lo, inv))], 1u);
     __syncwarp();
     int bstar, lt, midc;
-    find_split(h, nl, lane, bstar, lt, midc);
+    find_split<kBinsL>(h, nl, lane, bstar, lt, midc);
     const int take = nl - lt;
     int cl = 0, cm = 0, cr = 0;
     T a[2][3], z[2][3];
@@ -561,7 +610,7 @@ __global__ void __launch_bounds__(128) bucket_kd_leaves_kernel(const BucketBuild
         p3[1] = src.y[st + i];
         p3[2] = src.z[st + i];
         o = src.o[st + i];
-        const int bn = bin_of(ax == 0 ? p3[0] : (ax == 1 ? p3[1] : p3[2]), lo, inv);
+        const int bn = bin_of<kBinsL>(ax == 0 ? p3[0] : (ax == 1 ? p3[1] : p3[2]), lo, inv);
         cat = bn < bstar ? 0 : (bn == bstar ? 1 : 2);
       }
       const unsigned mk0 = __ballot_sync(0xffffffffu, cat == 0);
@@ -629,7 +678,7 @@ __global__ void __launch_bounds__(128) bucket_kd_leaves_kernel(const BucketBuild
 }
 
 // histograms of the CTA phase
-size_t bucket_kd_smem() { return (size_t)kMaxSeg * kBins * sizeof(uint32_t); }
+size_t bucket_kd_smem() { return (size_t)kMaxSeg * kBins1 * sizeof(uint32_t); }
 
 // largest segment the CTA phase hands over: the split sizes depend on n and
 // the bucket size only (left_size), so the host replays the level loop
@@ -668,7 +717,7 @@ cudaError_t launch_bucket_kd(int dtype, const BucketBuildParams& p, int64_t batc
   // leaf kernel: up to 4 warps (segments) per CTA with their segments staged
   // in shared memory; 2 or 1 for bigger segments; global arrays beyond that
   const int mmax = kd_max_segment(p.n, p.bs);
-  int cap = (mmax + 31) / 32 * 32, wpc = 4;
+  int cap = (mmax + 31) / 32 * 32, wpc = 8;
   while (wpc > 1 && (size_t)wpc * kd_leaves_warp_bytes(cap, esz) > (size_t)optin) wpc >>= 1;
   if ((size_t)wpc * kd_leaves_warp_bytes(cap, esz) > (size_t)optin) {
     cap = 0;
