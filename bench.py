@@ -475,9 +475,11 @@ def run_ours(args, rank: int, world: int, local_rank: int):
             "units_per_launch": units_launch, "bytes_per_unit": BYTES_PER_UNIT_F32,
             "peak_src": pk["src"],
             "note": ("algorithmic bytes of the standard streaming FPS (20 B per point-"
-                     "iteration = distance_evals) / greedy-kernel time; >1 because the state "
-                     "stays on chip / in L2 and the bucketed schedule skips provably "
-                     "unaffected buckets"),
+                     "iteration = distance_evals) / time of one greedy call on the launching "
+                     "stream (CUDA events around ffps_run_kernel: for K1b/K1m/K1g that is "
+                     "the K0 bucket build plus the greedy kernel, so the greedy kernel alone "
+                     "is faster than kernel_ms); >1 because the state stays on chip / in L2 "
+                     "and the bucketed schedules skip provably unaffected buckets"),
             "issue_bound": {"achieved_units_per_s": units_launch / (kms / 1e3),
                             "ceiling_units_per_s": issue_ceiling,
                             "frac": units_launch / (kms / 1e3) / issue_ceiling,
