@@ -291,6 +291,12 @@ bool make_bucket_plan(int dev, int dtype, int64_t n, BucketPlan* out, bool multi
   return false;
 }
 
+// bytes of the bucket-box array [batch][nb][6], rounded up to 256 so that the
+// arrays carved after it (O, TX..TO) stay 16-B aligned for the TMA staging of K0
+size_t box_bytes(int64_t nb, size_t esz, int64_t batch) {
+  return ((size_t)nb * 6 * esz * (size_t)batch + 255) / 256 * 256;
+}
+
 int run_bucketed(int dtype, const void* xyz, int64_t batch, int64_t cloud_stride, int64_t n,
                  int64_t iters, const int64_t* seed_pos, const int64_t* index_map,
                  int64_t map_stride, int64_t* order, void* sel_d2, int64_t out_stride,
@@ -307,7 +313,7 @@ int run_bucketed(int dtype, const void* xyz, int64_t batch, int64_t cloud_stride
   const size_t per_cloud = (size_t)nslots * (7 * esz + 8) + (size_t)bp.nbuckets * 6 * esz;
   unsigned char* scratch = nullptr;
   cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&scratch),
-                                  per_cloud * (size_t)batch + 256, st);
+                                  per_cloud * (size_t)batch + 512, st);
   if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync(buckets)");
   const size_t arr = (size_t)nslots * esz * (size_t)batch;
   ffps::BucketBuildParams bb;
@@ -321,8 +327,8 @@ int run_bucketed(int dtype, const void* xyz, int64_t batch, int64_t cloud_stride
   bb.Z = scratch + 2 * arr;
   bb.D = scratch + 3 * arr;
   bb.BB = scratch + 4 * arr;
-  bb.O = reinterpret_cast<int32_t*>(scratch + 4 * arr + (size_t)bp.nbuckets * 6 * esz *
-                                                            (size_t)batch);
+  bb.O = reinterpret_cast<int32_t*>(scratch + 4 * arr +
+                                    box_bytes(bp.nbuckets, esz, batch));
   bb.nslots = nslots;
   bb.nbuckets = bp.nbuckets;
   bb.bs = bs;
@@ -428,7 +434,7 @@ int run_grid(int dtype, const void* xyz, int64_t batch, int64_t cloud_stride, in
   const size_t per_cloud = (size_t)nslots * (7 * esz + 8) + (size_t)nb * 6 * esz;
   unsigned char* scratch = nullptr;
   cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&scratch),
-                                  per_cloud * (size_t)batch + 256, st);
+                                  per_cloud * (size_t)batch + 512, st);
   if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync(grid)");
   const size_t arr = (size_t)nslots * esz * (size_t)batch;
   ffps::BucketBuildParams bb;
@@ -442,7 +448,7 @@ int run_grid(int dtype, const void* xyz, int64_t batch, int64_t cloud_stride, in
   bb.Z = scratch + 2 * arr;
   bb.D = scratch + 3 * arr;
   bb.BB = scratch + 4 * arr;
-  bb.O = reinterpret_cast<int32_t*>(scratch + 4 * arr + (size_t)nb * 6 * esz * (size_t)batch);
+  bb.O = reinterpret_cast<int32_t*>(scratch + 4 * arr + box_bytes(nb, esz, batch));
   bb.nslots = nslots;
   bb.nbuckets = nb;
   bb.bs = bs;
@@ -764,7 +770,7 @@ int ffps_coverage(int dtype, const void* xyz, int64_t batch, int64_t cloud_strid
   const size_t per_p = (size_t)nsp * (7 * esz + 8) + (size_t)nbp * 6 * esz;
   const size_t per_s = (size_t)nss * (7 * esz + 8) + (size_t)nbs * 6 * esz;
   unsigned char* scratch = nullptr;
-  e = cudaMallocAsync(reinterpret_cast<void**>(&scratch), (per_p + per_s) * (size_t)batch + 512,
+  e = cudaMallocAsync(reinterpret_cast<void**>(&scratch), (per_p + per_s) * (size_t)batch + 1024,
                       st);
   if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync(coverage)");
   auto carve = [&](unsigned char* base, int64_t nslots, int64_t nb, int64_t bs,
@@ -775,7 +781,7 @@ int ffps_coverage(int dtype, const void* xyz, int64_t batch, int64_t cloud_strid
     bb.Z = base + 2 * arr;
     bb.D = base + 3 * arr;
     bb.BB = base + 4 * arr;
-    bb.O = reinterpret_cast<int32_t*>(base + 4 * arr + (size_t)nb * 6 * esz * (size_t)batch);
+    bb.O = reinterpret_cast<int32_t*>(base + 4 * arr + box_bytes(nb, esz, batch));
     bb.nslots = nslots;
     bb.nbuckets = nb;
     bb.bs = bs;
@@ -797,7 +803,7 @@ int ffps_coverage(int dtype, const void* xyz, int64_t batch, int64_t cloud_strid
   bs.index_map = idx;
   bs.map_stride = idx_stride;
   bs.n = m;
-  carve(scratch + per_p * (size_t)batch, nss, nbs, bss, bs);
+  carve(scratch + per_p * (size_t)batch + 256, nss, nbs, bss, bs);
   int launches = 0;
   e = ffps::launch_bucket_build(dtype, bp, batch, st);
   if (e == cudaSuccess) {

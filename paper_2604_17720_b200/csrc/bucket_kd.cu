@@ -34,6 +34,7 @@
 #include <vector>
 
 #include "ffps_internal.h"
+#include "ptx.cuh"
 
 namespace ffps {
 
@@ -150,7 +151,7 @@ __device__ __forceinline__ void find_split(const uint32_t* h, int nl, int lane, 
 // (start, size, parity, box) and, when staged, two SoA buffers of cap points
 __host__ __device__ constexpr size_t kd_leaves_warp_bytes(int cap, int esz) {
   return ((size_t)kBinsL * 4 + (size_t)kStack * 3 * 4 + (kStack & 1) * 4 + (size_t)kStack * 6 * esz +
-          (size_t)2 * cap * (3 * esz + 4) + 15) / 16 * 16;
+          16 /* staging mbarrier */ + (size_t)2 * cap * (3 * esz + 4) + 15) / 16 * 16;
 }
 
 template <typename T>
@@ -483,20 +484,45 @@ __global__ void __launch_bounds__(256) bucket_kd_leaves_kernel(const BucketBuild
   const int m0 = seg_sm[((int64_t)b * kMaxSeg + s0) * 2 + 1];
   Bufs<T> P0, P1;
   if (cap > 0) {
-    // stage the segment: P[k] points at buffer k minus st0, so global
-    // positions index it directly
-    T* A = w_box + kStack * 6;
+    // stage the segment with four TMA bulk copies (x, y, z, o; 16-B aligned:
+    // segments start on bucket boundaries, sizes rounded up inside the
+    // nslots-long arrays); P0 / P1 point at the buffers minus st0, so global
+    // positions index them directly
+    uint64_t* sbar = reinterpret_cast<uint64_t*>(w_box + kStack * 6);
+    T* A = reinterpret_cast<T*>(reinterpret_cast<unsigned char*>(sbar) + 16);
     const Bufs<T> src = par0 ? tmp : out;
     Bufs<T> bufA{A, A + cap, A + 2 * cap, reinterpret_cast<int32_t*>(A + 3 * cap)};
     Bufs<T> bufB{A + 3 * cap + cap * 4 / (int)sizeof(T), nullptr, nullptr, nullptr};
     bufB.y = bufB.x + cap;
     bufB.z = bufB.x + 2 * cap;
     bufB.o = reinterpret_cast<int32_t*>(bufB.x + 3 * cap);
-    for (int i = lane; i < m0; i += 32) {
-      bufA.x[i] = src.x[st0 + i];
-      bufA.y[i] = src.y[st0 + i];
-      bufA.z[i] = src.z[st0 + i];
-      bufA.o[i] = src.o[st0 + i];
+    {
+      const uint32_t bar = smem_u32(sbar);
+      const uint32_t bt = (uint32_t)(((size_t)m0 * sizeof(T) + 15) / 16 * 16);
+      const uint32_t bo = (uint32_t)(((size_t)m0 * 4 + 15) / 16 * 16);
+      const bool aligned = ((reinterpret_cast<uintptr_t>(src.x + st0) |
+                             reinterpret_cast<uintptr_t>(src.y + st0) |
+                             reinterpret_cast<uintptr_t>(src.z + st0) |
+                             reinterpret_cast<uintptr_t>(src.o + st0)) & 15) == 0;
+      if (!aligned) {  // carved arrays are 16-B aligned (abi.cu box_bytes); belt and braces
+        for (int i = lane; i < m0; i += 32) {
+          bufA.x[i] = src.x[st0 + i];
+          bufA.y[i] = src.y[st0 + i];
+          bufA.z[i] = src.z[st0 + i];
+          bufA.o[i] = src.o[st0 + i];
+        }
+        __syncwarp();
+      } else if (lane == 0) {
+        mbar_init(bar, 1);
+        fence_mbar_init_cta();
+        mbar_arrive_expect_tx(bar, 3 * bt + bo);
+        bulk_g2s(smem_u32(bufA.x), src.x + st0, bt, bar);
+        bulk_g2s(smem_u32(bufA.y), src.y + st0, bt, bar);
+        bulk_g2s(smem_u32(bufA.z), src.z + st0, bt, bar);
+        bulk_g2s(smem_u32(bufA.o), src.o + st0, bo, bar);
+      }
+      __syncwarp();
+      if (aligned) mbar_wait(bar, 0);
     }
     P0 = Bufs<T>{bufA.x - st0, bufA.y - st0, bufA.z - st0, bufA.o - st0};
     P1 = Bufs<T>{bufB.x - st0, bufB.y - st0, bufB.z - st0, bufB.o - st0};

@@ -108,4 +108,20 @@ __device__ __forceinline__ void prefetch_l1(const void* p) {
   asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
 }
 
+// TMA bulk copy (cp.async.bulk, 1-D) global -> this CTA's shared memory;
+// `bytes` (a multiple of 16, 16-B aligned addresses) complete on mbarrier `bar`
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes,
+                                         uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+      ::"r"(dst), "l"(src), "r"(bytes), "r"(bar)
+      : "memory");
+}
+
+// make an mbarrier initialised by this thread visible to the async proxy
+__device__ __forceinline__ void fence_mbar_init_cta() {
+  asm volatile("fence.mbarrier_init.release.cluster;\n\tfence.proxy.async.shared::cta;" :::
+                   "memory");
+}
+
 }  // namespace ffps
