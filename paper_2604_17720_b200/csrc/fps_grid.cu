@@ -69,7 +69,10 @@ constexpr WppTab make_wpp_tab() {
 __constant__ WppTab c_wpp = make_wpp_tab();
 // rounds re-test every bucket while the search radius is this large a fraction
 // of the cloud's extent (little to prune, the whole CTA shares the work)
-constexpr double kFullFrac = 0.375;
+#ifndef FFPS_GRID_FULLFRAC
+#define FFPS_GRID_FULLFRAC 0.375
+#endif
+constexpr double kFullFrac = FFPS_GRID_FULLFRAC;
 
 template <typename A>
 __device__ __forceinline__ int argmax_lane_g(typename A::bits_t v, uint32_t i) {
@@ -350,7 +353,8 @@ __global__ void __launch_bounds__(NT, 1) fps_grid_kernel(const BucketParams prm)
   };
   // warp-converged variant for two (point, bucket) tests per lane (two pairs of
   // the flag phase in flight): every lane calls it; new buckets are appended
-  // with one shared-memory atomic per warp and their points prefetched to L1
+  // with one shared-memory atomic per warp.  (An L2 -> L1 prefetch of the new
+  // buckets' points here was measured 3% slower and dropped.)
   auto test_warp2 = [&](bool v0, int q0, int t0, bool v1, int q1, int t1) {
     const bool h0 = v0 && !(box_lb(sp_w[0][t0][0], sp_w[0][t0][1], sp_w[0][t0][2],
                                    box + (size_t)q0 * 6) >= A::from_bits(kv[q0]));
@@ -358,20 +362,6 @@ __global__ void __launch_bounds__(NT, 1) fps_grid_kernel(const BucketParams prm)
                                    box + (size_t)q1 * 6) >= A::from_bits(kv[q1]));
     const bool n0 = h0 && atomicOr(&pmask[q0], 1u << t0) == 0u;
     const bool n1 = h1 && atomicOr(&pmask[q1], 1u << t1) == 0u;
-    auto prefetch = [&](int q) {  // re-evaluated after the barrier: start its L2 -> L1 fill
-      const int64_t s0 = ((int64_t)q * CL + rank) * BS;
-#pragma unroll
-      for (int u = 0; u < BS * (int)sizeof(T) / 128; ++u) {
-        prefetch_l1(X + s0 + u * (128 / sizeof(T)));
-        prefetch_l1(Y + s0 + u * (128 / sizeof(T)));
-        prefetch_l1(Z + s0 + u * (128 / sizeof(T)));
-        prefetch_l1(D + s0 + u * (128 / sizeof(T)));
-      }
-#pragma unroll
-      for (int u = 0; u < BS * 4 / 128; ++u) prefetch_l1(O + s0 + u * 32);
-    };
-    if (n0) prefetch(q0);
-    if (n1) prefetch(q1);
     const unsigned m0 = __ballot_sync(0xffffffffu, n0), m1 = __ballot_sync(0xffffffffu, n1);
     if (m0 | m1) {
       const int c0 = __popc(m0);
@@ -437,8 +427,13 @@ __global__ void __launch_bounds__(NT, 1) fps_grid_kernel(const BucketParams prm)
       __syncthreads();  // pair list complete
       // A2. all warps: the kGS buckets of every pair (one per lane)
       const int np = npair_s;
+#ifdef FFPS_GRID_ONEPAIR
+      for (int e = warp; e < np; e += NW) {
+        const bool two = false;
+#else
       for (int e = warp; e < np; e += 2 * NW) {
         const bool two = e + NW < np;
+#endif
         const int pr0 = pair_s[e], pr1 = two ? pair_s[e + NW] : pr0;
         const int q0 = (pr0 & 0xffff) * kGS + lane, q1 = (pr1 & 0xffff) * kGS + lane;
         test_warp2(q0 < nb, q0 < nb ? q0 : 0, pr0 >> 16, two && q1 < nb, q1 < nb ? q1 : 0,
@@ -524,7 +519,10 @@ __global__ void __launch_bounds__(NT, 1) fps_grid_kernel(const BucketParams prm)
     };
     {
       // all of a warp's buckets of the round in one batch when they fit
-      constexpr int CH = PPL <= 1 ? 4 : (PPL == 2 ? 2 : 1);  // <= 4 points per lane in flight
+#ifndef FFPS_GRID_CH1
+#define FFPS_GRID_CH1 4
+#endif
+      constexpr int CH = PPL <= 1 ? FFPS_GRID_CH1 : (PPL == 2 ? 2 : 1);  // <= 4 points per lane in flight
       for (int e = warp; e < nr; e += CH * NW) {
         const int nv = (nr - e + NW - 1) / NW;
         if (nv >= CH) batch(std::integral_constant<int, CH>{}, e);
