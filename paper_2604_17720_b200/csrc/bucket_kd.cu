@@ -31,6 +31,7 @@
 
 #include <cstdint>
 #include <cstdlib>
+#include <cstring>
 #include <vector>
 
 #include "ffps_internal.h"
@@ -162,7 +163,12 @@ struct Bufs {
 
 }  // namespace
 
-template <typename T>
+// CL = CTAs per cloud (thread-block cluster of 1 or 2): the points of every
+// pass are dealt over CL * kThreads threads; histograms and children boxes are
+// partial per CTA and summed through DSMEM (each rank reads its peer's partial
+// between two cluster barriers); the partition counters live in rank 0 and
+// are bumped with remote atomics; both ranks keep identical segment state.
+template <typename T, int CL>
 __global__ void __launch_bounds__(kThreads, 1) bucket_kd_kernel(const BucketBuildParams p,
                                                                 int32_t* seg_hdr, int32_t* seg_sm,
                                                                 T* seg_box) {
@@ -177,7 +183,21 @@ __global__ void __launch_bounds__(kThreads, 1) bucket_kd_kernel(const BucketBuil
   __shared__ I s_cbox[2 * kMaxSeg][6];  // boxes of their children
   __shared__ int s_S;
 
-  const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  static_assert(CL == 1 || CL == 2, "1 or 2 CTAs per cloud");
+  constexpr int GT = CL * kThreads;  // threads per cloud
+  const int rank = CL > 1 ? (int)cluster_ctarank() : 0;
+  const int b = (int)blockIdx.x / CL, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int gtid = rank * kThreads + tid;
+  const uint32_t peer = (uint32_t)(rank ^ 1);
+  auto ld_peer = [&](const I* local) -> I {  // the peer rank's copy of a shared word
+    const uint32_t a = mapa(smem_u32(local), peer);
+    if constexpr (sizeof(I) == 4) return (I)ld_cluster_u32(a);
+    else return (I)ld_cluster_u64(a);
+  };
+  auto sync_all = [&]() {
+    if constexpr (CL > 1) cluster_sync_all();
+    else __syncthreads();
+  };
   const int n = (int)p.n;
   const int bs = (int)p.bs;
   const T* X0 = static_cast<const T*>(p.xyz) + (int64_t)b * p.cloud_stride * 3;
@@ -197,18 +217,18 @@ __global__ void __launch_bounds__(kThreads, 1) bucket_kd_kernel(const BucketBuil
   __syncthreads();
   {
     T a[3] = {pinf, pinf, pinf}, z[3] = {-pinf, -pinf, -pinf};
-    for (int i0 = 0; i0 < n; i0 += kThreads * kU) {  // kU points per thread in flight
+    for (int i0 = 0; i0 < n; i0 += GT * kU) {  // kU points per thread in flight
       T v[kU][3];
 #pragma unroll
       for (int u = 0; u < kU; ++u) {
-        const int i = i0 + u * kThreads + tid;
+        const int i = i0 + u * GT + gtid;
         const int64_t s = i < n ? (map ? __ldg(map + i) : i) : 0;
 #pragma unroll
         for (int c = 0; c < 3; ++c) v[u][c] = i < n ? X0[3 * s + c] : T(0);
       }
 #pragma unroll
       for (int u = 0; u < kU; ++u) {
-        const int i = i0 + u * kThreads + tid;
+        const int i = i0 + u * GT + gtid;
         if (i < n) {
           out.x[i] = v[u][0];
           out.y[i] = v[u][1];
@@ -220,7 +240,7 @@ __global__ void __launch_bounds__(kThreads, 1) bucket_kd_kernel(const BucketBuil
       for (int u = 0; u < kU; ++u)
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
-        const bool in = i0 + u * kThreads + tid < n;
+        const bool in = i0 + u * GT + gtid < n;
         a[c] = in && v[u][c] < a[c] ? v[u][c] : a[c];
         z[c] = in && v[u][c] > z[c] ? v[u][c] : z[c];
       }
@@ -237,6 +257,14 @@ __global__ void __launch_bounds__(kThreads, 1) bucket_kd_kernel(const BucketBuil
         atomicMax(&s_box[0][3 + c], O::enc(z[c]));
       }
     }
+  }
+  if constexpr (CL > 1) {  // cloud box = both partial boxes
+    sync_all();
+    I pv = 0;
+    if (tid < 6) pv = ld_peer(&s_box[0][tid]);
+    sync_all();
+    if (tid < 6) s_box[0][tid] = tid < 3 ? (pv < s_box[0][tid] ? pv : s_box[0][tid])
+                                         : (pv > s_box[0][tid] ? pv : s_box[0][tid]);
   }
   if (tid == 0) {
     s_S = 1;
@@ -271,7 +299,7 @@ __global__ void __launch_bounds__(kThreads, 1) bucket_kd_kernel(const BucketBuil
       s_cbox[tid / 6][c] = c < 3 ? O::kMax : O::kMin;
     }
     for (int i = tid; i < S * kBins1; i += kThreads) hist[i] = 0u;
-    __syncthreads();
+    sync_all();  // rank 0's counters reset before any rank's partition atomics
     // histogram pass (segment-major: the whole CTA on one segment at a time)
     for (int s = 0; s < S; ++s) {
       if (s_m[s] <= bs) continue;
@@ -279,16 +307,32 @@ __global__ void __launch_bounds__(kThreads, 1) bucket_kd_kernel(const BucketBuil
       const T lo = s_lo[s], inv = s_inv[s];
       const T* v = ax == 0 ? src.x : (ax == 1 ? src.y : src.z);
       uint32_t* h = hist + s * kBins1;
-      for (int i0 = 0; i0 < m; i0 += kThreads * kU) {  // kU loads in flight, then the atomics
+      for (int i0 = 0; i0 < m; i0 += GT * kU) {  // kU loads in flight, then the atomics
         T w[kU];
 #pragma unroll
         for (int u = 0; u < kU; ++u) {
-          const int i = i0 + u * kThreads + tid;
+          const int i = i0 + u * GT + gtid;
           w[u] = i < m ? v[st + i] : T(0);
         }
 #pragma unroll
         for (int u = 0; u < kU; ++u)
-          if (i0 + u * kThreads + tid < m) atomicAdd(&h[haddr<kBins1>(bin_of<kBins1>(w[u], lo, inv))], 1u);
+          if (i0 + u * GT + gtid < m) atomicAdd(&h[haddr<kBins1>(bin_of<kBins1>(w[u], lo, inv))], 1u);
+      }
+    }
+    if constexpr (CL > 1) {  // histograms = both partial histograms
+      constexpr int kW = kMaxSeg * kBins1 / kThreads;  // words per thread at most
+      uint32_t pv[kW];
+      sync_all();
+#pragma unroll
+      for (int k = 0; k < kW; ++k) {
+        const int i = k * kThreads + tid;
+        pv[k] = i < S * kBins1 ? ld_cluster_u32(mapa(smem_u32(&hist[i]), peer)) : 0u;
+      }
+      sync_all();
+#pragma unroll
+      for (int k = 0; k < kW; ++k) {
+        const int i = k * kThreads + tid;
+        if (i < S * kBins1) hist[i] += pv[k];
       }
     }
     __syncthreads();
@@ -320,12 +364,12 @@ __global__ void __launch_bounds__(kThreads, 1) bucket_kd_kernel(const BucketBuil
           a[k][c] = pinf;
           z[k][c] = -pinf;
         }
-      for (int j0 = 0; j0 < m; j0 += kThreads * kU) {  // warp-uniform trip count
+      for (int j0 = 0; j0 < m; j0 += GT * kU) {  // warp-uniform trip count
        T vv[kU][3];
        int32_t oo[kU];
 #pragma unroll
        for (int u = 0; u < kU; ++u) {  // kU points per thread in flight
-         const int i = j0 + u * kThreads + tid;
+         const int i = j0 + u * GT + gtid;
          const bool live = i < m;
          vv[u][0] = live ? src.x[st + i] : T(0);
          vv[u][1] = live ? src.y[st + i] : T(0);
@@ -334,7 +378,7 @@ __global__ void __launch_bounds__(kThreads, 1) bucket_kd_kernel(const BucketBuil
        }
 #pragma unroll
        for (int u = 0; u < kU; ++u) {
-        const int i = j0 + u * kThreads + tid;
+        const int i = j0 + u * GT + gtid;
         const bool live = i < m;
         const T v[3] = {vv[u][0], vv[u][1], vv[u][2]};
         const int32_t o = oo[u];
@@ -355,7 +399,13 @@ __global__ void __launch_bounds__(kThreads, 1) bucket_kd_kernel(const BucketBuil
             if (!mk) continue;
             const int ldr = __ffs(mk) - 1;
             int basek = 0;
-            if (lane == ldr) basek = atomicAdd(k == 0 ? &s_cl[s] : (k == 1 ? &s_cm[s] : &s_cr[s]), __popc(mk));
+            if (lane == ldr) {
+              int* ctr = k == 0 ? &s_cl[s] : (k == 1 ? &s_cm[s] : &s_cr[s]);
+              if constexpr (CL > 1)  // counters of rank 0 (positions global over the cluster)
+                basek = (int)atom_add_cluster(mapa(smem_u32(ctr), 0u), (uint32_t)__popc(mk));
+              else
+                basek = atomicAdd(ctr, __popc(mk));
+            }
             basek = __shfl_sync(0xffffffffu, basek, ldr);
             if (cat == k) {
               const int t = basek + __popc(mk & ((1u << lane) - 1u));
@@ -396,6 +446,17 @@ __global__ void __launch_bounds__(kThreads, 1) bucket_kd_kernel(const BucketBuil
           }
         }
     }
+    if constexpr (CL > 1) {  // children boxes = both partial boxes
+      sync_all();  // also: every rank's partition atomics done
+      I pv = 0;
+      const bool mine = tid < 2 * S * 6;
+      if (mine) pv = ld_peer(&s_cbox[tid / 6][tid % 6]);
+      sync_all();
+      if (mine) {
+        I& o = s_cbox[tid / 6][tid % 6];
+        o = tid % 6 < 3 ? (pv < o ? pv : o) : (pv > o ? pv : o);
+      }
+    }
     __syncthreads();
     // next level's segment list (children in order; unsplit segments carried)
     if (tid == 0) {
@@ -429,6 +490,7 @@ __global__ void __launch_bounds__(kThreads, 1) bucket_kd_kernel(const BucketBuil
 
   // 2. hand the segments to the leaf kernel: count, parity of the buffer that
   //    holds them, (start, size) and box of each
+  if (rank != 0) return;
   if (tid == 0) {
     seg_hdr[2 * b + 0] = s_S;
     seg_hdr[2 * b + 1] = par;
@@ -765,8 +827,17 @@ cudaError_t launch_bucket_kd(int dtype, const BucketBuildParams& p, int64_t batc
   int32_t* seg_hdr = reinterpret_cast<int32_t*>(segs);
   int32_t* seg_sm = reinterpret_cast<int32_t*>(segs + hdr_b);
   void* seg_box = segs + ((hdr_b + sm_b + 15) / 16) * 16;
-  const void* f1 = dtype == 0 ? reinterpret_cast<const void*>(&bucket_kd_kernel<float>)
-                              : reinterpret_cast<const void*>(&bucket_kd_kernel<double>);
+  // CTA phase: 2 CTAs per cloud (a cluster) while the batch fits the SMs twice
+  int sms = 0;
+  e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (e != cudaSuccess) return e;
+  int cl = batch * 2 <= sms ? 2 : 1;
+  if (const char* v = getenv("FFPS_KD_CL"))  // A/B: 1 or 2
+    if (atoi(v) == 1 || atoi(v) == 2) cl = atoi(v);
+  const void* f1 = dtype == 0 ? (cl == 2 ? reinterpret_cast<const void*>(&bucket_kd_kernel<float, 2>)
+                                         : reinterpret_cast<const void*>(&bucket_kd_kernel<float, 1>))
+                              : (cl == 2 ? reinterpret_cast<const void*>(&bucket_kd_kernel<double, 2>)
+                                         : reinterpret_cast<const void*>(&bucket_kd_kernel<double, 1>));
   const void* f2 = dtype == 0 ? reinterpret_cast<const void*>(&bucket_kd_leaves_kernel<float>)
                               : reinterpret_cast<const void*>(&bucket_kd_leaves_kernel<double>);
   e = cudaFuncSetAttribute(f1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bucket_kd_smem());
@@ -774,7 +845,20 @@ cudaError_t launch_bucket_kd(int dtype, const BucketBuildParams& p, int64_t batc
     e = cudaFuncSetAttribute(f2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)leaves_smem);
   if (e == cudaSuccess) {
     void* a1[] = {const_cast<BucketBuildParams*>(&p), &seg_hdr, &seg_sm, &seg_box};
-    e = cudaLaunchKernel(f1, dim3((unsigned)batch), dim3(kThreads), a1, bucket_kd_smem(), st);
+    cudaLaunchConfig_t cfg;
+    memset(&cfg, 0, sizeof cfg);
+    cfg.gridDim = dim3((unsigned)(batch * cl), 1, 1);
+    cfg.blockDim = dim3(kThreads, 1, 1);
+    cfg.dynamicSmemBytes = bucket_kd_smem();
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = cl;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    e = cudaLaunchKernelExC(&cfg, f1, a1);
   }
   if (e == cudaSuccess) {
     void* a2[] = {const_cast<BucketBuildParams*>(&p), &seg_hdr, &seg_sm, &seg_box, &cap, &wpc};
