@@ -611,9 +611,9 @@ __global__ void __launch_bounds__(256) bucket_kd_leaves_kernel(const BucketBuild
     const Bufs<T> src = pr ? P1 : P0, dst = pr ? P0 : P1;
     if (m <= bs) {
       // leaf = bucket q: into the output arrays (unless it already is there),
-      // D = +inf, box; the last bucket also gets its padding slots
+      // D = +inf; its box is the exact min/max the split (or the CTA phase)
+      // computed for it; the last bucket also gets its padding slots
       const bool copy = src.x + st != out.x + st;
-      T a[3] = {pinf, pinf, pinf}, z[3] = {-pinf, -pinf, -pinf};
       T f0 = T(0), f1 = T(0), f2 = T(0);
       for (int i = lane; i < m; i += 32) {
         const T v0 = src.x[st + i], v1 = src.y[st + i], v2 = src.z[st + i];
@@ -629,26 +629,11 @@ __global__ void __launch_bounds__(256) bucket_kd_leaves_kernel(const BucketBuild
           f1 = v1;
           f2 = v2;
         }
-        a[0] = v0 < a[0] ? v0 : a[0];
-        a[1] = v1 < a[1] ? v1 : a[1];
-        a[2] = v2 < a[2] ? v2 : a[2];
-        z[0] = v0 > z[0] ? v0 : z[0];
-        z[1] = v1 > z[1] ? v1 : z[1];
-        z[2] = v2 > z[2] ? v2 : z[2];
-      }
-#pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        a[c] = wmin(a[c]);
-        z[c] = wmax(z[c]);
       }
       const int q = st / bs;
-      if (lane == 0) {
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-          BB[(int64_t)q * 6 + c] = a[c];
-          BB[(int64_t)q * 6 + 3 + c] = z[c];
-        }
-      }
+      const T bl = lane == 0 ? bx[0] : lane == 1 ? bx[1] : lane == 2 ? bx[2]
+                 : lane == 3 ? bx[3] : lane == 4 ? bx[4] : bx[5];  // no dynamic index
+      if (lane < 6) BB[(int64_t)q * 6 + lane] = bl;
       if (st + m == n && (int64_t)n < p.nslots) {
         f0 = __shfl_sync(0xffffffffu, f0, 0);
         f1 = __shfl_sync(0xffffffffu, f1, 0);
