@@ -131,3 +131,22 @@ def test_host_pipeline_matches_device_pipeline(chunks):
         assert torch.equal(gi, w.indices.cpu()) and torch.equal(gs, w.selection_dist2.cpu())
         assert fb == w.fill_boundary
     assert tot_g.distance_evals == tot_w.distance_evals and tot_g.cache_bytes == tot_w.cache_bytes
+
+
+@pytest.mark.parametrize("sched", ["stream", "grid"])
+def test_flash_stage1_full_shape_fp64_bit_exact(sched):
+    """binary64 — the reference's own precision: the C5 FlashFPS
+    stage-1 run (50,000 candidates, 12,500 iterations) equals the oracle's
+    binary64 restatement of run_kernel bit for bit."""
+    prev = _device.set_schedule(sched)
+    try:
+        N, budgets = SHAPES["C5"]
+        cfg = ffps.PruneConfig(p=0.75)
+        k, c = cfg.kernel_budget(budgets[0]), min(cfg.candidate_count(N, budgets[0]), N)
+        x = _uniform(2, N, 300).astype(np.float64)
+        seeds = np.array([0, 4242])
+        go, gs = _greedy(x, c, k, seeds)
+        wo, ws = oracle.run_kernel_batch(x, k, seeds, n=c)
+        _assert_same(go, gs, wo, ws, f"C5 fp64 {sched}")
+    finally:
+        _device.set_schedule(prev)
