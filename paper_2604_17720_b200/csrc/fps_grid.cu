@@ -218,6 +218,7 @@ __global__ void __launch_bounds__(NT, 1) fps_grid_kernel(const BucketParams prm)
   __shared__ int16_t top_s[KM];  // rows of the ranked top-KM candidates
   __shared__ bits_t topv_s[KM];
   __shared__ int topg_s[KM];     // the KM groups with the best maxima (phase R1)
+  __shared__ int16_t grank_s[128];  // group -> its rank among them, -1 (general path)
   __shared__ int ngv_s;          // non-empty groups (phase R1)
   __shared__ int rr_s[KM * NCG];  // phase R2 ranks (0x7fffffff: empty)
   // phase R1 -> R2: the candidates of the top-KM groups, group rank major
@@ -543,6 +544,7 @@ __global__ void __launch_bounds__(NT, 1) fps_grid_kernel(const BucketParams prm)
     //    (only the groups with a re-evaluated bucket changed: the dirty list)
     if (tid < KM * NCG) compv_s[tid] = A::kmin;  // R1 fills the ranks it finds
     if (tid < KM) topg_s[tid] = -1;              // ranks of empty groups stay -1
+    if (tid < ng) grank_s[tid] = -1;             // R1 sets the top groups' ranks
     for (int wd = 0, base = 0; wd < ((ng + 31) >> 5); ++wd) {
       const unsigned mword = dmask_s[wd];
       const int cw = __popc(mword);
@@ -600,6 +602,7 @@ __global__ void __launch_bounds__(NT, 1) fps_grid_kernel(const BucketParams prm)
         if (part == 0 && v != A::kmin) {
           if (cnt < KM) {
             topg_s[cnt] = g;
+            grank_s[g] = (int16_t)cnt;
 #pragma unroll
             for (int k = 0; k < NCG; ++k) {
               compv_s[cnt * NCG + k] = cand_v[NCG * g + k];
@@ -668,12 +671,33 @@ __global__ void __launch_bounds__(NT, 1) fps_grid_kernel(const BucketParams prm)
         nl = nvalid < KM ? nvalid : KM;
         if (lane < nl) top_w[0][lane] = top_s[lane];
       } else {
+        // every key >= tau2: (a) the candidates of the top groups whose
+        // (NCG+1)-th key is below tau2 (all their keys >= tau2 are candidates),
+        // (b) all keys >= tau2 of the top groups that overflow and of any other
+        // group whose max reaches tau2 (exact ties with the KM-th candidate)
         nct = 0;
+        const unsigned ovf = __ballot_sync(0xffffffffu, lane < ngt && tn != A::kmin && tn >= tau2);
+#pragma unroll
+        for (int c0 = 0; c0 < KM * NCG; c0 += 32) {
+          const int c = c0 + lane;
+          const bits_t v = c < nrc ? compv_s[c] : A::kmin;
+          const bool take = c < nrc && !((ovf >> (c / NCG)) & 1u) && v != A::kmin && v >= tau2;
+          const unsigned cm = __ballot_sync(0xffffffffu, take);
+          const int slot = nct + __popc(cm & below);
+          if (take && slot < 64) {
+            cv_w[0][slot] = v;
+            ci_w[0][slot] = compp_s[c];
+            cq_w[0][slot] = (int16_t)compq_s[c];
+          }
+          nct += __popc(cm);
+        }
 #pragma unroll 1
         for (int j = 0; j < (ng + 31) / 32; ++j) {
           const int gj = j * 32 + lane;
           const bits_t gvj = gj < ng ? gmax[gj] : A::kmin;
-          unsigned hm = __ballot_sync(0xffffffffu, gvj >= tau2 && gvj != A::kmin);
+          const int grk = gj < ng ? grank_s[gj] : -1;  // rank among the top groups, -1: none
+          const bool scan = grk < 0 || ((ovf >> grk) & 1u);
+          unsigned hm = __ballot_sync(0xffffffffu, gvj >= tau2 && gvj != A::kmin && scan);
           while (hm) {
             const int q = (j * 32 + __ffs(hm) - 1) * kGS + lane;
             hm &= hm - 1u;
@@ -705,6 +729,19 @@ __global__ void __launch_bounds__(NT, 1) fps_grid_kernel(const BucketParams prm)
           if (lane == 0) top_w[0][0] = (int16_t)qmax;
           nl = 1;
           trunc = true;
+        } else if (nct <= 32) {  // one entry per lane: ranks by shuffles
+          const bool live = lane < nct;
+          const bits_t v = live ? cv_w[0][lane] : A::kmin;
+          const uint32_t i = live ? ci_w[0][lane] : kNoIdx;
+          int r3 = 0;
+#pragma unroll
+          for (int e = 0; e < 32; ++e) {
+            const bits_t ve = A::shfl(v, e);
+            const uint32_t ie = __shfl_sync(0xffffffffu, i, e);
+            r3 += (e < nct && (ve > v || (ve == v && ie < i))) ? 1 : 0;
+          }
+          if (live && r3 < KM) top_w[0][r3] = cq_w[0][lane];
+          nl = nct < KM ? nct : KM;
         } else {
 #pragma unroll
           for (int h = 0; h < 2; ++h) {  // entries lane and lane + 32
