@@ -199,8 +199,10 @@ __global__ void __launch_bounds__(NT, 1) fps_grid_kernel(const BucketParams prm)
 #ifndef FFPS_GRID_NCG16
 #define FFPS_GRID_NCG16 4
 #endif
-  // candidates per group (A/B: FFPS_GRID_NCG16 for KM = 16)
+  // candidates per group (A/B: FFPS_GRID_NCG16 for KM = 16, at most 4: the
+  // per-group shared-memory layout of grid_smem_bytes holds 4)
   constexpr int NCG = KM == 16 ? FFPS_GRID_NCG16 : (KM < 16 ? KM / 4 : 4);
+  static_assert(NCG >= 1 && NCG <= 4, "grid_smem_bytes sizes 4 candidates per group");
   bits_t* gmax = k2 + nb;                                // [ng] group max key
   bits_t* gnext = gmax + ng;                             // [ng]
   bits_t* cand_v = gnext + ng;                           // [NCG ng]
