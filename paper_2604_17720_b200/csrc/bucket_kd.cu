@@ -165,9 +165,10 @@ struct Bufs {
 
 // CL = CTAs per cloud (thread-block cluster of 1 or 2): the points of every
 // pass are dealt over CL * kThreads threads; histograms and children boxes are
-// partial per CTA and summed through DSMEM (each rank reads its peer's partial
-// between two cluster barriers); the partition counters live in rank 0 and
-// are bumped with remote atomics; both ranks keep identical segment state.
+// partial per CTA and summed through DSMEM; rank 1 places its points after
+// rank 0's in every category (rank 0's counts come from its partial
+// histogram), so the partition needs no remote atomics; both ranks keep
+// identical segment state.
 template <typename T, int CL>
 __global__ void __launch_bounds__(kThreads, 1) bucket_kd_kernel(const BucketBuildParams p,
                                                                 int32_t* seg_hdr, int32_t* seg_sm,
@@ -299,7 +300,7 @@ __global__ void __launch_bounds__(kThreads, 1) bucket_kd_kernel(const BucketBuil
       s_cbox[tid / 6][c] = c < 3 ? O::kMax : O::kMin;
     }
     for (int i = tid; i < S * kBins1; i += kThreads) hist[i] = 0u;
-    sync_all();  // rank 0's counters reset before any rank's partition atomics
+    __syncthreads();
     // histogram pass (segment-major: the whole CTA on one segment at a time)
     for (int s = 0; s < S; ++s) {
       if (s_m[s] <= bs) continue;
@@ -319,32 +320,51 @@ __global__ void __launch_bounds__(kThreads, 1) bucket_kd_kernel(const BucketBuil
           if (i0 + u * GT + gtid < m) atomicAdd(&h[haddr<kBins1>(bin_of<kBins1>(w[u], lo, inv))], 1u);
       }
     }
-    if constexpr (CL > 1) {  // histograms = both partial histograms
-      constexpr int kW = kMaxSeg * kBins1 / kThreads;  // words per thread at most
-      uint32_t pv[kW];
+    // CL > 1: each rank keeps its partial histogram (first half of `hist`,
+    // S <= kMaxSeg / 2 inside the loop) and builds the total in the second
+    // half; the peer only ever reads the partials, which stay untouched until
+    // the next level
+    constexpr int kHalf = kMaxSeg / 2 * kBins1;
+    if constexpr (CL > 1) {
       sync_all();
-#pragma unroll
-      for (int k = 0; k < kW; ++k) {
-        const int i = k * kThreads + tid;
-        pv[k] = i < S * kBins1 ? ld_cluster_u32(mapa(smem_u32(&hist[i]), peer)) : 0u;
-      }
-      sync_all();
-#pragma unroll
-      for (int k = 0; k < kW; ++k) {
-        const int i = k * kThreads + tid;
-        if (i < S * kBins1) hist[i] += pv[k];
-      }
+      for (int i = tid; i < S * kBins1; i += kThreads)
+        hist[kHalf + i] = hist[i] + ld_cluster_u32(mapa(smem_u32(&hist[i]), peer));
     }
     __syncthreads();
     for (int sw = warp; sw < S; sw += kNW) {
       if (s_m[sw] <= bs) continue;
       int bstar, before, mid;
-      find_split<kBins1>(hist + sw * kBins1, s_nl[sw], lane, bstar, before, mid);
+      const uint32_t* ht = hist + (CL > 1 ? kHalf : 0) + sw * kBins1;
+      find_split<kBins1>(ht, s_nl[sw], lane, bstar, before, mid);
       if (lane == 0) {
         s_b[sw] = bstar;
         s_lt[sw] = before;
         s_mid[sw] = mid;
         s_take[sw] = s_nl[sw] - before;
+      }
+      if constexpr (CL > 1) {
+        // rank 0's points of each category (its partial histogram: its own
+        // half, or total - own for rank 1) -> rank 1's counters start there,
+        // so both ranks place their points with local atomics only
+        constexpr int BPL = kBins1 / 32;
+        const uint32_t* hp = hist + sw * kBins1;
+        uint32_t below = 0, at = 0, all = 0;
+#pragma unroll
+        for (int j = 0; j < BPL; ++j) {
+          const int bin = BPL * lane + j, w = j * 32 + lane;
+          const uint32_t a0 = rank == 0 ? hp[w] : ht[w] - hp[w];
+          all += a0;
+          below += bin < bstar ? a0 : 0u;
+          at += bin == bstar ? a0 : 0u;
+        }
+        below = __reduce_add_sync(0xffffffffu, below);
+        at = __reduce_add_sync(0xffffffffu, at);
+        all = __reduce_add_sync(0xffffffffu, all);
+        if (lane == 0 && rank == 1) {
+          s_cl[sw] = (int)below;
+          s_cm[sw] = (int)at;
+          s_cr[sw] = (int)(all - below - at);
+        }
       }
     }
     __syncthreads();
@@ -399,13 +419,8 @@ __global__ void __launch_bounds__(kThreads, 1) bucket_kd_kernel(const BucketBuil
             if (!mk) continue;
             const int ldr = __ffs(mk) - 1;
             int basek = 0;
-            if (lane == ldr) {
-              int* ctr = k == 0 ? &s_cl[s] : (k == 1 ? &s_cm[s] : &s_cr[s]);
-              if constexpr (CL > 1)  // counters of rank 0 (positions global over the cluster)
-                basek = (int)atom_add_cluster(mapa(smem_u32(ctr), 0u), (uint32_t)__popc(mk));
-              else
-                basek = atomicAdd(ctr, __popc(mk));
-            }
+            if (lane == ldr)  // rank 1's counters start after rank 0's points
+              basek = atomicAdd(k == 0 ? &s_cl[s] : (k == 1 ? &s_cm[s] : &s_cr[s]), __popc(mk));
             basek = __shfl_sync(0xffffffffu, basek, ldr);
             if (cat == k) {
               const int t = basek + __popc(mk & ((1u << lane) - 1u));
