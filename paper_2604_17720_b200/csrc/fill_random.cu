@@ -14,7 +14,8 @@
 //   1. selection bitmap of [0, n) and the zero count before every word (block
 //      scan) — the pool as ranks;
 //   2. thread 0 runs the generator; the tail shuffle works on a window of
-//      kWin steps: draws first, then all 2 * kWin loads in flight, aliasing
+//      kWin steps (8: larger windows thrash the instruction cache): draws
+//      first, then all 2 * kWin loads in flight, aliasing
 //      inside the window resolved in registers, then the stores (the only
 //      reads a step can see from earlier steps of the window are the slots
 //      they wrote, j_a == j_b or j_a == i_b);
@@ -31,7 +32,10 @@ namespace ffps {
 namespace {
 
 constexpr int kRThreads = 512;
-constexpr int kWin = 16;
+#ifndef FFPS_FILL_WIN
+#define FFPS_FILL_WIN 8
+#endif
+constexpr int kWin = FFPS_FILL_WIN;  // tail shuffle: steps per window
 
 struct Pcg64 {
   uint64_t hi, lo, ihi, ilo;
@@ -59,7 +63,11 @@ struct Pcg64 {
     return (uint32_t)v;
   }
   // random_bounded_uint64(off = 0, rng, mask = 0, use_masked = false), rng < 2^32
+#ifdef FFPS_FILL_NOINLINE
+  __device__ __noinline__ uint32_t bounded(uint32_t rng) {
+#else
   __device__ uint32_t bounded(uint32_t rng) {
+#endif
     if (rng == 0u) return 0u;
     if (rng == 0xffffffffu) return next32();
     const uint32_t excl = rng + 1u;
