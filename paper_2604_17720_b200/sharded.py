@@ -6,7 +6,7 @@ split across GPUs; every rank samples its own contiguous slice of the batch
 with the single-GPU kernels and there is NO data-path collective.  The only
 exchange is the final index gather of layer-1 indices (layers 2..L are prefix
 views of layer 1 when the cache is on, so only layer 1 moves): an
-``all_gather_into_tensor`` of (B_r, M1) int64 per rank.
+``all_gather_into_tensor`` of (B_r, M1) indices per rank, sent as int32.
 
 The reference has no multi-device code; the per-cloud
 semantics are those of hierarchical_sample (fps_cache.py:204-240).
@@ -36,6 +36,7 @@ def shard_range(batch: int, world: int, rank: int) -> tuple[int, int]:
 
 def gather_rows(local: torch.Tensor, batch: int, group=None) -> torch.Tensor:
     """Concatenate every rank's (B_r, ...) rows in rank order into (batch, ...).
+    int64 rows are point indices (< 2^31) and travel as int32.
 
     Shards are padded to the largest shard so the collective is a single
     ``all_gather_into_tensor`` (NCCL); on backends without it (gloo) the list
@@ -43,11 +44,13 @@ def gather_rows(local: torch.Tensor, batch: int, group=None) -> torch.Tensor:
     with NCCL (production)."""
     world = dist.get_world_size(group)
     rows = -(-batch // world) if batch else 0
-    pad = torch.zeros((rows,) + tuple(local.shape[1:]), dtype=local.dtype,
-                      device=local.device)
+    # int64 point indices travel as int32 (clouds hold < 2^31 points): half
+    # the bytes on the wire; the result is int64 again
+    wire = torch.int32 if local.dtype == torch.int64 else local.dtype
+    pad = torch.zeros((rows,) + tuple(local.shape[1:]), dtype=wire, device=local.device)
     pad[: local.shape[0]].copy_(local)
     if dist.get_backend(group) == "nccl":
-        out = torch.empty((world * rows,) + tuple(local.shape[1:]), dtype=local.dtype,
+        out = torch.empty((world * rows,) + tuple(local.shape[1:]), dtype=wire,
                           device=local.device)
         dist.all_gather_into_tensor(out, pad, group=group)
         parts = list(out.split(rows)) if rows else [out] * world
@@ -60,7 +63,7 @@ def gather_rows(local: torch.Tensor, batch: int, group=None) -> torch.Tensor:
     for r in range(world):
         lo, hi = shard_range(batch, world, r)
         keep.append(parts[r][: hi - lo])
-    return torch.cat(keep, 0)
+    return torch.cat(keep, 0).to(local.dtype)
 
 
 def hierarchical_sample_sharded(xyz_local, budgets: Sequence[int], cfg: PruneConfig,
