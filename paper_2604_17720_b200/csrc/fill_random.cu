@@ -84,7 +84,64 @@ struct Pcg64 {
   }
 };
 
+// 128-bit LCG arithmetic for the jump-ahead of the PCG64 state
+struct U128 {
+  uint64_t hi, lo;
+};
+__device__ __forceinline__ U128 mul128(U128 a, U128 b) {  // low 128 bits of a * b
+  return U128{__umul64hi(a.lo, b.lo) + a.lo * b.hi + a.hi * b.lo, a.lo * b.lo};
+}
+__device__ __forceinline__ U128 add128(U128 a, U128 b) {
+  const uint64_t lo = a.lo + b.lo;
+  return U128{a.hi + b.hi + (lo < a.lo ? 1ull : 0ull), lo};
+}
+__device__ __forceinline__ uint64_t pcg_output(U128 s) {  // XSL-RR
+  const uint64_t x = s.hi ^ s.lo;
+  const unsigned r = (unsigned)(s.hi >> 58);
+  return r ? (x >> r) | (x << (64u - r)) : x;
+}
+constexpr uint64_t kMulHi = 2549297995355413924ull, kMulLo = 4865540595714422341ull;
+
+// 32-bit values the generator will hand out, in order ([lo(o1), hi(o1),
+// lo(o2), ...]: pcg64_next32 returns the low half of a fresh output and
+// buffers the high half): nv / 2 outputs, lane l computes outputs l+1, l+33, ...
+// by jumping 32 LCG steps at a time
+__device__ void pcg_stream(uint32_t* v, int64_t nv, U128 s0, U128 inc, int lane,
+                           uint64_t* sh_hi, uint64_t* sh_lo) {
+  const U128 M{kMulHi, kMulLo};
+  if (lane == 0) {  // states after 1..32 steps
+    U128 st = s0;
+    for (int l = 0; l < 32; ++l) {
+      st = add128(mul128(st, M), inc);
+      sh_hi[l] = st.hi;
+      sh_lo[l] = st.lo;
+    }
+  }
+  __syncwarp();
+  U128 st{sh_hi[lane], sh_lo[lane]};
+  U128 A = M, C = inc;  // (A, C) of 32 steps: s -> A s + C
+#pragma unroll
+  for (int r = 0; r < 5; ++r) {
+    C = add128(mul128(A, C), C);
+    A = mul128(A, A);
+  }
+  for (int64_t o = lane; o < nv / 2; o += 32) {
+    const uint64_t x = pcg_output(st);
+    v[2 * o] = (uint32_t)x;
+    v[2 * o + 1] = (uint32_t)(x >> 32);
+    st = add128(mul128(A, st), C);
+  }
+  __syncwarp();
+}
+
 }  // namespace
+
+// stream values allotted to a tail shuffle of nsteps draws: one per draw plus
+// room for Lemire rejections (each costs one more value; expected count
+// nsteps * pop / 2^32), rounded to whole warps of outputs
+__host__ __device__ inline int64_t fill_stream_values(int64_t nsteps) {
+  return ((nsteps + nsteps / 8 + 4096) + 63) / 64 * 64;
+}
 
 __global__ void __launch_bounds__(kRThreads) fill_random_kernel(
     int64_t* order_all, void* sel_all, int f64, int64_t out_stride, int64_t n, int64_t k,
@@ -96,7 +153,7 @@ __global__ void __launch_bounds__(kRThreads) fill_random_kernel(
   const int64_t W = (n + 31) / 32;
   uint32_t* bitmap = scratch + (int64_t)blockIdx.x * scratch_words;
   uint32_t* zrank = bitmap + W;   // [W + 1]
-  uint32_t* work = zrank + W + 1;  // tail: data[pop]; Floyd: hash set [mask + 1]
+  uint32_t* work = zrank + W + 1;  // tail: data[pop], drawn j [pop]; Floyd: hash set [mask + 1]
   const int64_t pop = n - k, size = m1 - k;
   const bool tail = pop > 10000 && size > pop / 50;
   uint64_t mask = 0;
@@ -159,43 +216,105 @@ __global__ void __launch_bounds__(kRThreads) fill_random_kernel(
     if (w_lo < W && w_hi == W) zrank[W] = run;
   }
 
-  // 2. the generator (thread 0): pool ranks into order[k, m1)
-  if (tid == 0) {
-    Pcg64 g{s_hi, s_lo, i_hi, i_lo, false, 0u};
-    int64_t* out = order + k;
-    if (tail) {
-      const int64_t first = (pop - size) > 1 ? (pop - size) : 1;
-      for (int64_t i0 = pop - 1; i0 >= first; i0 -= kWin) {
-        const int cnt = (i0 - first + 1) < kWin ? (int)(i0 - first + 1) : kWin;
-        uint32_t iu[kWin], ju[kWin], vj[kWin], vi[kWin];
-#pragma unroll
-        for (int u = 0; u < kWin; ++u) {
-          iu[u] = (uint32_t)(i0 - u);
-          ju[u] = u < cnt ? g.bounded(iu[u]) : 0u;
+  // 2. the generator: pool ranks into order[k, m1)
+  int64_t* out = order + k;
+  if (tail) {
+    // tail partial Fisher-Yates: warp 0 produces the generator's values with
+    // a 32-step jump-ahead per lane and maps them to the draws (Lemire's
+    // rejections shift later draws by one value), then applies the swaps 32
+    // steps at a time: all 64 loads in flight, the in-batch aliasing resolved by a scan
+    // in step order (step b sees the slots written by steps a < b), one store
+    // per slot by its last writer
+    const int64_t first = (pop - size) > 1 ? (pop - size) : 1;
+    const int64_t nsteps = pop - first;  // steps i = pop - 1, ..., first
+    uint32_t* jarr = work + pop;          // [nsteps] drawn j of step t (i = pop - 1 - t)
+    uint32_t* vstr = jarr + nsteps;       // [nv] the generator's 32-bit values
+    const int64_t nv = fill_stream_values(nsteps);
+    __shared__ uint64_t sh_hi[32], sh_lo[32];
+    __shared__ int s_ovf;
+    if (warp == 0) {
+      pcg_stream(vstr, nv, U128{s_hi, s_lo}, U128{i_hi, i_lo}, lane, sh_hi, sh_lo);
+      // draws -> values, 32 at a time: draw t takes value P + (t - t0) unless
+      // an earlier draw of the batch was rejected; the first rejected draw is
+      // redrawn by lane 0 and the next batch starts after it
+      int64_t t0 = 0, P = 0;
+      int ovf = 0;
+      while (t0 < nsteps) {
+        if (P + 32 > nv) {
+          ovf = 1;
+          break;
         }
-#pragma unroll
-        for (int u = 0; u < kWin; ++u) {
-          vj[u] = u < cnt ? work[ju[u]] : 0u;
-          vi[u] = u < cnt ? work[iu[u]] : 0u;
+        const int64_t t = t0 + lane;
+        const bool live = t < nsteps;
+        const uint32_t rng = live ? (uint32_t)(pop - 1 - t) : 1u, excl = rng + 1u;
+        const uint64_t m = (uint64_t)vstr[P + lane] * excl;
+        const uint32_t left = (uint32_t)m;
+        bool rej = false;
+        if (live && left < excl) rej = left < (0xffffffffu - rng) % excl;
+        const unsigned rm = __ballot_sync(0xffffffffu, rej);
+        const int f = rm ? __ffs(rm) - 1 : 32;
+        if (live && lane < f) jarr[t] = (uint32_t)(m >> 32);
+        if (f == 32) {
+          t0 += 32;
+          P += 32;
+          continue;
         }
-#pragma unroll
-        for (int b = 0; b < kWin; ++b) {
-#pragma unroll
-          for (int a = 0; a < b; ++a) {  // slots written earlier in the window
-            if (ju[a] == ju[b]) vj[b] = vi[a];
-            if (ju[a] == iu[b]) vi[b] = vi[a];
-          }
-          // step b: out = data[j]; data[j] = data[i] (vi[b] now holds the value
-          // written to slot j_b, read by later steps through the checks above)
-          const uint32_t o = vj[b];
-          if (b < cnt) out[iu[b] - (pop - size)] = o;
+        int64_t p = P + f;
+        if (lane == 0) {
+          const uint32_t rf = (uint32_t)(pop - 1 - (t0 + f)), ef = rf + 1u;
+          const uint32_t thr = (0xffffffffu - rf) % ef;
+          uint64_t mm = 0;
+          uint32_t lf = 0;
+          do {
+            ++p;
+            if (p >= nv) break;
+            mm = (uint64_t)vstr[p] * ef;
+            lf = (uint32_t)mm;
+          } while (lf < thr);
+          if (p < nv) jarr[t0 + f] = (uint32_t)(mm >> 32);
         }
-#pragma unroll
-        for (int b = 0; b < kWin; ++b)
-          if (b < cnt) work[ju[b]] = vi[b];
+        p = __shfl_sync(0xffffffffu, p, 0);
+        if (p >= nv) {
+          ovf = 1;
+          break;
+        }
+        t0 += f + 1;
+        P = p + 1;
       }
-      if (first > pop - size) out[0] = work[0];  // pop == size: slot 0 keeps its value
-    } else {
+      if (lane == 0) s_ovf = ovf;
+    }
+    __syncthreads();
+    if (s_ovf && tid == 0) {  // more rejections than the stream allots: draw sequentially
+      Pcg64 g{s_hi, s_lo, i_hi, i_lo, false, 0u};
+      for (int64_t t = 0; t < nsteps; ++t) jarr[t] = g.bounded((uint32_t)(pop - 1 - t));
+    }
+    __syncthreads();
+    if (warp == 0) {
+      for (int64_t t0 = 0; t0 < nsteps; t0 += 32) {
+        const int64_t t = t0 + lane;
+        const bool live = t < nsteps;
+        const uint32_t i = (uint32_t)(pop - 1 - (live ? t : 0));
+        const uint32_t j = live ? jarr[t] : 0xffffffffu;
+        uint32_t vj = live ? work[j] : 0u, vi = live ? work[i] : 0u;
+#pragma unroll 4
+        for (int a = 0; a < 31; ++a) {
+          const uint32_t ja = __shfl_sync(0xffffffffu, j, a);
+          const uint32_t wa = __shfl_sync(0xffffffffu, vi, a);  // value step a writes to slot ja
+          if (lane > a) {
+            if (j == ja) vj = wa;
+            if (i == ja) vi = wa;
+          }
+        }
+        if (live) out[i - (pop - size)] = vj;  // step: out = data[j]; data[j] = data[i]
+        const unsigned same = __match_any_sync(0xffffffffu, j);
+        if (live && lane == 31 - __clz(same)) work[j] = vi;
+        __syncwarp();
+      }
+      if (lane == 0 && first > pop - size) out[0] = work[0];  // pop == size: slot 0 stays
+    }
+  } else if (tid == 0) {
+    Pcg64 g{s_hi, s_lo, i_hi, i_lo, false, 0u};
+    {
       // Floyd's algorithm, hash set of mask + 1 slots (empty = 0xffffffff)
       for (int64_t j = pop - size; j < pop; ++j) {
         const uint32_t val = g.bounded((uint32_t)j);
@@ -246,7 +365,8 @@ __global__ void __launch_bounds__(kRThreads) fill_random_kernel(
 
 int64_t fill_random_scratch_words(int64_t n, int64_t k, int64_t m1) {
   const int64_t W = (n + 31) / 32, pop = n - k, size = m1 - k;
-  int64_t work = pop;
+  const int64_t nsteps = pop - ((pop - size) > 1 ? (pop - size) : 1);
+  int64_t work = pop + nsteps + fill_stream_values(nsteps);  // data, drawn j, values
   if (!(pop > 10000 && size > pop / 50)) {
     uint64_t mask = (uint64_t)(1.2 * (double)size);
     mask |= mask >> 1; mask |= mask >> 2; mask |= mask >> 4;
