@@ -13,12 +13,13 @@
 // reference seeds a fresh generator per call):
 //   1. selection bitmap of [0, n) and the zero count before every word (block
 //      scan) — the pool as ranks;
-//   2. thread 0 runs the generator; the tail shuffle works on a window of
-//      kWin steps (8: larger windows thrash the instruction cache): draws
-//      first, then all 2 * kWin loads in flight, aliasing
-//      inside the window resolved in registers, then the stores (the only
-//      reads a step can see from earlier steps of the window are the slots
-//      they wrote, j_a == j_b or j_a == i_b);
+//   2. warp 0 runs the generator: the 32-bit value stream by a 32-step
+//      jump-ahead of the 128-bit LCG per lane, the values mapped to draws 32
+//      at a time (a Lemire rejection cuts the batch and shifts the later draws
+//      by one value), then the tail shuffle 32 steps per batch (64 loads in
+//      flight, in-batch aliasing resolved by a scan in step order, one store
+//      per slot by its last writer); Floyd's branch (small fills) runs on
+//      thread 0;
 //   3. all threads map the drawn pool ranks to cloud indices (binary search of
 //      the word prefix, then the rank-th zero bit of the word).
 #include <cuda_runtime.h>
@@ -32,10 +33,6 @@ namespace ffps {
 namespace {
 
 constexpr int kRThreads = 512;
-#ifndef FFPS_FILL_WIN
-#define FFPS_FILL_WIN 8
-#endif
-constexpr int kWin = FFPS_FILL_WIN;  // tail shuffle: steps per window
 
 struct Pcg64 {
   uint64_t hi, lo, ihi, ilo;
@@ -63,11 +60,7 @@ struct Pcg64 {
     return (uint32_t)v;
   }
   // random_bounded_uint64(off = 0, rng, mask = 0, use_masked = false), rng < 2^32
-#ifdef FFPS_FILL_NOINLINE
-  __device__ __noinline__ uint32_t bounded(uint32_t rng) {
-#else
   __device__ uint32_t bounded(uint32_t rng) {
-#endif
     if (rng == 0u) return 0u;
     if (rng == 0xffffffffu) return next32();
     const uint32_t excl = rng + 1u;
