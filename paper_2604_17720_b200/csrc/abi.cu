@@ -875,8 +875,11 @@ int ffps_fill_random(int dtype, int64_t* order, void* sel_d2, int64_t batch, int
                                   (size_t)words * 4 * (size_t)batch, st);
   if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync(fill_random)");
   const uint64_t pcg[4] = {state_hi, state_lo, inc_hi, inc_lo};
+  // FFPS_FILL_SEQUENTIAL=1 (tests): the single-thread generator that backs up
+  // the warp-parallel one when Lemire rejections outrun its value stream
+  const char* seq = getenv("FFPS_FILL_SEQUENTIAL");
   e = ffps::launch_fill_random(dtype, order, sel_d2, batch, out_stride, n, k, m1, pcg, scratch,
-                               st);
+                               st, seq && strcmp(seq, "1") == 0);
   cudaError_t e2 = cudaFreeAsync(scratch, st);
   if (e != cudaSuccess) return cuda_fail(e, "fill_random_kernel launch");
   if (e2 != cudaSuccess) return cuda_fail(e2, "cudaFreeAsync(fill_random)");

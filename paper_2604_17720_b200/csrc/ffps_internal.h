@@ -141,6 +141,7 @@ cudaError_t launch_fill_slice(int dtype, int64_t* order, void* sel_d2, int64_t b
 int64_t fill_random_scratch_words(int64_t n, int64_t k, int64_t m1);
 cudaError_t launch_fill_random(int dtype, int64_t* order, void* sel_d2, int64_t batch,
                                int64_t out_stride, int64_t n, int64_t k, int64_t m1,
-                               const uint64_t pcg[4], uint32_t* scratch, cudaStream_t st);
+                               const uint64_t pcg[4], uint32_t* scratch, cudaStream_t st,
+                               bool sequential = false);
 
 }  // namespace ffps

@@ -139,7 +139,7 @@ __host__ __device__ inline int64_t fill_stream_values(int64_t nsteps) {
 __global__ void __launch_bounds__(kRThreads) fill_random_kernel(
     int64_t* order_all, void* sel_all, int f64, int64_t out_stride, int64_t n, int64_t k,
     int64_t m1, uint64_t s_hi, uint64_t s_lo, uint64_t i_hi, uint64_t i_lo, uint32_t* scratch,
-    int64_t scratch_words) {
+    int64_t scratch_words, int sequential) {
   __shared__ int64_t warp_tot[kRThreads / 32];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   int64_t* order = order_all + (int64_t)blockIdx.x * out_stride;
@@ -225,7 +225,9 @@ __global__ void __launch_bounds__(kRThreads) fill_random_kernel(
     const int64_t nv = fill_stream_values(nsteps);
     __shared__ uint64_t sh_hi[32], sh_lo[32];
     __shared__ int s_ovf;
-    if (warp == 0) {
+    if (warp == 0 && sequential) {
+      if (lane == 0) s_ovf = 1;  // test hook: the sequential generator below
+    } else if (warp == 0) {
       pcg_stream(vstr, nv, U128{s_hi, s_lo}, U128{i_hi, i_lo}, lane, sh_hi, sh_lo);
       // draws -> values, 32 at a time: draw t takes value P + (t - t0) unless
       // an earlier draw of the batch was rejected; the first rejected draw is
@@ -371,11 +373,12 @@ int64_t fill_random_scratch_words(int64_t n, int64_t k, int64_t m1) {
 
 cudaError_t launch_fill_random(int dtype, int64_t* order, void* sel_d2, int64_t batch,
                                int64_t out_stride, int64_t n, int64_t k, int64_t m1,
-                               const uint64_t pcg[4], uint32_t* scratch, cudaStream_t st) {
+                               const uint64_t pcg[4], uint32_t* scratch, cudaStream_t st,
+                               bool sequential) {
   if (m1 - k <= 0 || batch <= 0) return cudaSuccess;
   fill_random_kernel<<<(unsigned)batch, kRThreads, 0, st>>>(
       order, sel_d2, dtype == 1, out_stride, n, k, m1, pcg[0], pcg[1], pcg[2], pcg[3], scratch,
-      fill_random_scratch_words(n, k, m1));
+      fill_random_scratch_words(n, k, m1), sequential ? 1 : 0);
   return cudaGetLastError();
 }
 

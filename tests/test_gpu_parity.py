@@ -327,10 +327,15 @@ def test_multi_winner_degenerate_ties(cuda, dtype, sched):
     (60000, 1100, 0.05, 2),      # Floyd with pop > 10000, fill <= pop // 50
     (3000, 3000, 0.5, 7),        # Floyd with pop == fill
 ])
-def test_seeded_random_fill_matches_numpy(cuda, n, m1, p, rng_seed, dtype):
+@pytest.mark.parametrize("sequential", [False, True])
+def test_seeded_random_fill_matches_numpy(cuda, n, m1, p, rng_seed, dtype, sequential,
+                                          monkeypatch):
     """K2r: FillMode.SEEDED_RANDOM on the device equals
     np.random.default_rng(rng_seed).choice(pool, m1 - k, replace=False) of the
-    reference (fps_prune.py:96-103) for every cloud, bit for bit."""
+    reference (fps_prune.py:96-103) for every cloud, bit for bit — through the
+    warp-parallel generator and through its sequential backup."""
+    if sequential:
+        monkeypatch.setenv("FFPS_FILL_SEQUENTIAL", "1")
     rng = np.random.default_rng(41)
     B = 3
     pts = rng.random((B, n, 3)).astype(dtype)
