@@ -351,3 +351,25 @@ def test_seeded_random_fill_matches_numpy(cuda, n, m1, p, rng_seed, dtype, seque
                                                       replace=False)
         assert np.array_equal(idx[b, k:], want), (n, m1, p, b)
         assert (sel[b, k:] == 0).all()
+
+
+@pytest.mark.parametrize("kd", ["cl1", "cl2", "global"])
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+def test_kd_bucket_build_variants(cuda, kd, dtype, monkeypatch):
+    """K0-kd in each configuration — CTA phase on one CTA or a 2-CTA cluster
+    (FFPS_KD_CL), leaf phase staged in shared memory or on the global arrays
+    (FFPS_KD_STAGE=0) — feeds K1g with the same exact results, including a
+    batch too large for 2 CTAs per cloud, restricted (index-mapped) runs and
+    ragged sizes around the bucket size."""
+    if kd == "global":
+        monkeypatch.setenv("FFPS_KD_STAGE", "0")
+    else:
+        monkeypatch.setenv("FFPS_KD_CL", kd[-1])
+    with _Sched("grid"):
+        rng = np.random.default_rng(29)
+        for N, m, B, kind in [(31, 31, 3, "uniform"), (65, 40, 2, "ties"), (3000, 700, 80, "uniform"),
+                              (20000, 900, 2, "ties"), (60000, 500, 2, "uniform")]:
+            _check_batch(_cloud(rng, B, N, kind, dtype), min(m, N), rng.integers(0, N, size=B))
+        xyz = _cloud(rng, 2, 9000, "uniform", dtype)
+        imap = np.stack([rng.permutation(9000)[:5000] for _ in range(2)])
+        _check_batch(xyz, 800, np.array([0, 17]), index_map=imap)
