@@ -95,6 +95,23 @@ __device__ __forceinline__ T wmax(T v) {
   }
   return v;
 }
+// box reductions: one REDUX on the order-preserving integer image for float
+// (five shuffles otherwise; -0 orders below +0, which the bounds tolerate:
+// they compare equal in every use)
+template <typename T>
+__device__ __forceinline__ T bmin(T v) {
+  if constexpr (sizeof(T) == 4)
+    return Ord<T>::dec(__reduce_min_sync(0xffffffffu, Ord<T>::enc(v)));
+  else
+    return wmin(v);
+}
+template <typename T>
+__device__ __forceinline__ T bmax(T v) {
+  if constexpr (sizeof(T) == 4)
+    return Ord<T>::dec(__reduce_max_sync(0xffffffffu, Ord<T>::enc(v)));
+  else
+    return wmax(v);
+}
 
 template <int NB, typename T>
 __device__ __forceinline__ int bin_of(T v, T lo, T inv) {
@@ -248,8 +265,8 @@ __global__ void __launch_bounds__(kThreads, 1) bucket_kd_kernel(const BucketBuil
     }
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
-      a[c] = wmin(a[c]);
-      z[c] = wmax(z[c]);
+      a[c] = bmin(a[c]);
+      z[c] = bmax(z[c]);
     }
     if (lane == 0) {
 #pragma unroll
@@ -454,7 +471,7 @@ __global__ void __launch_bounds__(kThreads, 1) bucket_kd_kernel(const BucketBuil
       for (int k = 0; k < 2; ++k)
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
-          const T mn = wmin(a[k][c]), mx = wmax(z[k][c]);
+          const T mn = bmin(a[k][c]), mx = bmax(z[k][c]);
           if (lane == 0 && mn <= mx) {
             atomicMin(&s_cbox[2 * s + k][c], O::enc(mn));
             atomicMax(&s_cbox[2 * s + k][3 + c], O::enc(mx));
@@ -738,8 +755,8 @@ __global__ void __launch_bounds__(256) bucket_kd_leaves_kernel(const BucketBuild
     for (int k = 0; k < 2; ++k)
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
-        a[k][c] = wmin(a[k][c]);
-        z[k][c] = wmax(z[k][c]);
+        a[k][c] = bmin(a[k][c]);
+        z[k][c] = bmax(z[k][c]);
       }
     if (top + 2 > kStack) __trap();  // depth <= log2(n / BS) + 1 < kStack
     if (lane == 0) {  // push right then left (left processed first; order is irrelevant)
