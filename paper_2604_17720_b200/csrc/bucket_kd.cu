@@ -468,15 +468,17 @@ __global__ void __launch_bounds__(kThreads, 1) bucket_kd_kernel(const BucketBuil
        }
       }
 #pragma unroll
-      for (int k = 0; k < 2; ++k)
+      for (int k = 0; k < 2; ++k) {
+        if (!__any_sync(0xffffffffu, a[k][0] <= z[k][0])) continue;  // no point of child k
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
           const T mn = bmin(a[k][c]), mx = bmax(z[k][c]);
-          if (lane == 0 && mn <= mx) {
+          if (lane == 0) {
             atomicMin(&s_cbox[2 * s + k][c], O::enc(mn));
             atomicMax(&s_cbox[2 * s + k][3 + c], O::enc(mx));
           }
         }
+      }
     }
     if constexpr (CL > 1) {  // children boxes = both partial boxes
       sync_all();  // also: every rank's partition atomics done
