@@ -89,14 +89,18 @@ int ffps_run_kernel(int dtype, const void* xyz, int64_t batch,
  *                     each cloud's buckets are split over a cluster of 1, 2 or
  *                     4 CTAs: FFPS_ALGO_GRID_CL(c) fixes c, plain FFPS_ALGO_GRID
  *                     takes 2 for n >= 20000 while batch * 2 <= SM count, else 1;
+ *   FFPS_ALGO_SMALL   K1s: clouds of up to 8192 points, one CTA per cloud, points in
+ *                     registers, one barrier per greedy step (larger clouds fall
+ *                     back to STREAM);
  *   FFPS_ALGO_AUTO    GRID for n >= 16384 (any batch) or n >= 12288 with >= 16
  *                     clouds, 2 CTAs per cloud from n >= 20000 while the
  *                     batch fits the SMs twice; BUCKET for smaller clouds when
- *                     the batch fills the GPU; else STREAM (the environment
- *                     variable FFPS_ALGO=stream|bucket|multi|grid overrides
+ *                     the batch fills the GPU; SMALL for n <= 4096; else
+ *                     STREAM (the environment variable
+ *                     FFPS_ALGO=stream|small|bucket|multi|grid overrides
  *                     AUTO). */
 enum ffps_algo { FFPS_ALGO_AUTO = 0, FFPS_ALGO_STREAM = 1, FFPS_ALGO_BUCKET = 2,
-                 FFPS_ALGO_MULTI = 3, FFPS_ALGO_GRID = 4 };
+                 FFPS_ALGO_MULTI = 3, FFPS_ALGO_GRID = 4, FFPS_ALGO_SMALL = 5 };
 #define FFPS_ALGO_GRID_CL(c) (FFPS_ALGO_GRID | ((c) << 8))
 
 /* Host -> device copy of the candidate prefix xyz[b][0:n_prefix) of every

@@ -535,6 +535,42 @@ int run_grid(int dtype, const void* xyz, int64_t batch, int64_t cloud_stride, in
   return FFPS_OK;
 }
 
+// K1s: clouds of up to 8192 points, one CTA per cloud (fps_small.cu); the
+// smallest thread count / points-per-thread pair that holds n
+int run_small(int dtype, const void* xyz, int64_t batch, int64_t cloud_stride, int64_t n,
+              int64_t iters, const int64_t* seed_pos, const int64_t* index_map,
+              int64_t map_stride, int64_t* order, void* sel_d2, int64_t out_stride,
+              cudaStream_t st) {
+  int cnt = 0;
+  const ffps::SmallInst* insts = ffps::small_instances(&cnt);
+  const ffps::SmallInst* pick = nullptr;
+  for (int i = 0; i < cnt; ++i) {
+    const auto& k = insts[i];
+    if (k.dtype != dtype || (int64_t)k.nt * k.q < n) continue;
+    const int64_t cap = (int64_t)k.nt * k.q, pcap = pick ? (int64_t)pick->nt * pick->q : 0;
+    if (!pick || cap < pcap || (cap == pcap && k.nt > pick->nt)) pick = &k;  // fewer slots per thread
+  }
+  if (!pick) return fail(FFPS_EUNSUPPORTED, "no small-cloud configuration for n=%lld", (long long)n);
+  ffps::GreedyParams prm;
+  memset(&prm, 0, sizeof prm);
+  prm.xyz = xyz;
+  prm.cloud_stride = cloud_stride;
+  prm.index_map = index_map;
+  prm.map_stride = map_stride;
+  prm.n = n;
+  prm.iters = iters;
+  prm.seed_pos = seed_pos;
+  prm.order = order;
+  prm.sel_d2 = sel_d2;
+  prm.out_stride = out_stride;
+  prm.neg_zero = -0.0f;
+  void* args[] = {&prm};
+  cudaError_t e = cudaLaunchKernel(pick->fn, dim3((unsigned)batch), dim3(pick->nt), args, 0, st);
+  if (e != cudaSuccess) return cuda_fail(e, "fps_small_kernel launch");
+  g_last_launches = 1;
+  return FFPS_OK;
+}
+
 int run_streaming(int dtype, const void* xyz, int64_t batch, int64_t cloud_stride, int64_t n,
                   int64_t iters, const int64_t* seed_pos, const int64_t* index_map,
                   int64_t map_stride, int64_t* order, void* sel_d2, int64_t out_stride,
@@ -613,10 +649,15 @@ int run_streaming(int dtype, const void* xyz, int64_t batch, int64_t cloud_strid
 //          points, and >= 12K points once >= 16 clouds;
 //   BUCKET (one CTA per cloud, exact bucket bounds) for smaller clouds when the
 //          batch fills the GPU (>= 48 clouds of >= 6K points, >= 96 of >= 3K);
+//   SMALL  (one CTA per cloud, points in registers) for clouds of <= 4096
+//          points (tools/sweep_stream_small.py);
 //   STREAM (clusters of up to 16 CTAs, every point every iteration) otherwise.
-// FFPS_ALGO in the environment ("stream" / "bucket" / "multi" / "grid")
-// overrides AUTO.
+// FFPS_ALGO in the environment ("stream" / "small" / "bucket" / "multi" /
+// "grid") overrides AUTO.
+constexpr int64_t kSmallMax = 8192;  // K1s: points per cloud at most
+
 int auto_algo(int64_t n, int64_t batch) {
+  if (n <= 4096) return FFPS_ALGO_SMALL;  // tools/sweep_stream_small.py: 1.2-2x the others
   if (n >= 16384 || (n >= 12288 && batch >= 16)) return FFPS_ALGO_GRID;
   if ((n >= 6144 && batch >= 48) || (n >= 3072 && batch >= 96)) return FFPS_ALGO_BUCKET;
   return FFPS_ALGO_STREAM;
@@ -631,6 +672,7 @@ int resolve_algo(int algo, int64_t n, int64_t batch) {
     if (env && strcmp(env, "bucket") == 0) return FFPS_ALGO_BUCKET;
     if (env && strcmp(env, "multi") == 0) return FFPS_ALGO_MULTI;
     if (env && strcmp(env, "grid") == 0) return FFPS_ALGO_GRID;
+    if (env && strcmp(env, "small") == 0) return FFPS_ALGO_SMALL;
     return auto_algo(n, batch);
   }
   return algo;
@@ -708,7 +750,7 @@ int ffps_run_kernel_ex(int dtype, const void* xyz, int64_t batch, int64_t cloud_
     return fail(FFPS_EINVAL, "dtype must be FFPS_F32 or FFPS_F64");
   if (algo != FFPS_ALGO_AUTO && algo != FFPS_ALGO_STREAM && algo != FFPS_ALGO_BUCKET &&
       algo != FFPS_ALGO_MULTI && algo != FFPS_ALGO_GRID && algo != FFPS_ALGO_GRID_CL(1) &&
-      algo != FFPS_ALGO_GRID_CL(2) && algo != FFPS_ALGO_GRID_CL(4))
+      algo != FFPS_ALGO_GRID_CL(2) && algo != FFPS_ALGO_GRID_CL(4) && algo != FFPS_ALGO_SMALL)
     return fail(FFPS_EINVAL, "unknown algorithm %d", algo);
   if (batch < 0) return fail(FFPS_EINVAL, "batch=%lld < 0", (long long)batch);
   if (batch == 0) return FFPS_OK;
@@ -731,6 +773,9 @@ int ffps_run_kernel_ex(int dtype, const void* xyz, int64_t batch, int64_t cloud_
   if (a == FFPS_ALGO_BUCKET || a == FFPS_ALGO_MULTI)
     return run_bucketed(dtype, xyz, batch, cloud_stride, n, iters, seed_pos, index_map,
                         map_stride, order, sel_d2, out_stride, st, dev, a == FFPS_ALGO_MULTI);
+  if (a == FFPS_ALGO_SMALL && n <= kSmallMax)  // larger clouds: the streaming kernel
+    return run_small(dtype, xyz, batch, cloud_stride, n, iters, seed_pos, index_map, map_stride,
+                     order, sel_d2, out_stride, st);
   return run_streaming(dtype, xyz, batch, cloud_stride, n, iters, seed_pos, index_map,
                        map_stride, order, sel_d2, out_stride, st, dev);
 }

@@ -27,6 +27,16 @@ struct GreedyParams {
   int64_t trace_iters;
 };
 
+// K1s: one compiled configuration of the small-cloud kernel (fps_small.cu):
+// nt threads per CTA, q points per thread (n <= nt * q), one CTA per cloud.
+struct SmallInst {
+  int dtype;  // 0 f32, 1 f64
+  int nt;
+  int q;
+  const void* fn;
+};
+const SmallInst* small_instances(int* count);
+
 // One compiled configuration of the greedy kernel.
 struct KernelInst {
   int dtype;  // 0 f32, 1 f64

@@ -40,13 +40,14 @@ class _Sched:
             os.environ["FFPS_GRID_KM"] = self.prev_km
 
 
-SCHEDULES = ["stream", "bucket", "multi", "grid", "grid@1", "grid@2", "grid@2/km8"]
+SCHEDULES = ["stream", "small", "bucket", "multi", "grid", "grid@1", "grid@2", "grid@2/km8"]
 
 
 @pytest.fixture(params=SCHEDULES)
 def schedule(request):
-    """Run the test under each greedy schedule (K1 streaming, K0+K1b bucketed,
-    K1m multi-winner, K1g cell-indexed with 1/2/4 CTAs per cloud)."""
+    """Run the test under each greedy schedule (K1 streaming, K1s small-cloud
+    (n <= 8192, else streaming), K0+K1b bucketed, K1m multi-winner, K1g with 1/2
+    CTAs per cloud)."""
     with _Sched(request.param):
         yield request.param
 
