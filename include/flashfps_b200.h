@@ -95,7 +95,7 @@ int ffps_run_kernel(int dtype, const void* xyz, int64_t batch,
  *   FFPS_ALGO_AUTO    GRID for n >= 16384 (any batch) or n >= 12288 with >= 16
  *                     clouds, 2 CTAs per cloud from n >= 20000 while the
  *                     batch fits the SMs twice; BUCKET for smaller clouds when
- *                     the batch fills the GPU; SMALL for n <= 4096; else
+ *                     the batch fills the GPU; SMALL for n <= 8192; else
  *                     STREAM (the environment variable
  *                     FFPS_ALGO=stream|small|bucket|multi|grid overrides
  *                     AUTO). */

@@ -544,9 +544,15 @@ int run_small(int dtype, const void* xyz, int64_t batch, int64_t cloud_stride, i
   int cnt = 0;
   const ffps::SmallInst* insts = ffps::small_instances(&cnt);
   const ffps::SmallInst* pick = nullptr;
+  int fnt = 0, fq = 0;  // FFPS_SMALL_PLAN="nt,q" (sweeps)
+  if (const char* v = getenv("FFPS_SMALL_PLAN")) sscanf(v, "%d,%d", &fnt, &fq);
   for (int i = 0; i < cnt; ++i) {
     const auto& k = insts[i];
     if (k.dtype != dtype || (int64_t)k.nt * k.q < n) continue;
+    if (fnt) {
+      if (k.nt == fnt && k.q == fq) pick = &k;
+      continue;
+    }
     const int64_t cap = (int64_t)k.nt * k.q, pcap = pick ? (int64_t)pick->nt * pick->q : 0;
     if (!pick || cap < pcap || (cap == pcap && k.nt > pick->nt)) pick = &k;  // fewer slots per thread
   }
@@ -564,8 +570,11 @@ int run_small(int dtype, const void* xyz, int64_t batch, int64_t cloud_stride, i
   prm.sel_d2 = sel_d2;
   prm.out_stride = out_stride;
   prm.neg_zero = -0.0f;
+  cudaError_t e = cudaFuncSetAttribute(pick->fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)pick->smem);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(small)");
   void* args[] = {&prm};
-  cudaError_t e = cudaLaunchKernel(pick->fn, dim3((unsigned)batch), dim3(pick->nt), args, 0, st);
+  e = cudaLaunchKernel(pick->fn, dim3((unsigned)batch), dim3(pick->nt), args, pick->smem, st);
   if (e != cudaSuccess) return cuda_fail(e, "fps_small_kernel launch");
   g_last_launches = 1;
   return FFPS_OK;
@@ -649,15 +658,15 @@ int run_streaming(int dtype, const void* xyz, int64_t batch, int64_t cloud_strid
 //          points, and >= 12K points once >= 16 clouds;
 //   BUCKET (one CTA per cloud, exact bucket bounds) for smaller clouds when the
 //          batch fills the GPU (>= 48 clouds of >= 6K points, >= 96 of >= 3K);
-//   SMALL  (one CTA per cloud, points in registers) for clouds of <= 4096
-//          points (tools/sweep_stream_small.py);
+//   SMALL  (one CTA per cloud, points in registers) for clouds of <= 8192
+//          points (tools/sweep_small.py, tools/sweep_stream_small.py);
 //   STREAM (clusters of up to 16 CTAs, every point every iteration) otherwise.
 // FFPS_ALGO in the environment ("stream" / "small" / "bucket" / "multi" /
 // "grid") overrides AUTO.
 constexpr int64_t kSmallMax = 8192;  // K1s: points per cloud at most
 
 int auto_algo(int64_t n, int64_t batch) {
-  if (n <= 4096) return FFPS_ALGO_SMALL;  // tools/sweep_stream_small.py: 1.2-2x the others
+  if (n <= kSmallMax) return FFPS_ALGO_SMALL;  // tools/sweep_small.py: 1.2-2x the others
   if (n >= 16384 || (n >= 12288 && batch >= 16)) return FFPS_ALGO_GRID;
   if ((n >= 6144 && batch >= 48) || (n >= 3072 && batch >= 96)) return FFPS_ALGO_BUCKET;
   return FFPS_ALGO_STREAM;

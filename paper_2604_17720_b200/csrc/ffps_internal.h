@@ -34,6 +34,7 @@ struct SmallInst {
   int nt;
   int q;
   const void* fn;
+  size_t smem;  // dynamic shared memory (the shared copy of the points)
 };
 const SmallInst* small_instances(int* count);
 

@@ -29,7 +29,6 @@ template <typename T>
 struct SmallRec {
   typename Arith<T>::bits_t v;
   uint32_t pos;
-  T x, y, z;
 };
 
 // dist update of one slot pair (f32: packed FADD2 / FFMA2 with -0 addend)
@@ -74,6 +73,12 @@ __global__ void __launch_bounds__(NT, 1) fps_small_kernel(const GreedyParams prm
   int64_t* order = prm.order + (int64_t)b * prm.out_stride;
   T* sel = static_cast<T*>(prm.sel_d2) + (int64_t)b * prm.out_stride;
   __shared__ SmallRec<T> rec[2][NW];
+  // a shared copy of the points: the step's winner is read from it by
+  // position, so the argmax carries (value, position) only
+  extern __shared__ __align__(16) unsigned char small_smem[];
+  T* sx = reinterpret_cast<T*>(small_smem);
+  T* sy = sx + NT * Q;
+  T* sz = sy + NT * Q;
 
   // points (fps_core.py:119-122); slots past n hold -inf and never win
   T x[Q], y[Q], z[Q], d[Q];
@@ -86,6 +91,9 @@ __global__ void __launch_bounds__(NT, 1) fps_small_kernel(const GreedyParams prm
     y[u] = in ? X0[3 * s + 1] : T(0);
     z[u] = in ? X0[3 * s + 2] : T(0);
     d[u] = in ? A::pinf() : A::ninf();
+    sx[pos] = x[u];
+    sy[pos] = y[u];
+    sz[pos] = z[u];
   }
   // seed (fps_core.py:124-130)
   const int seed = (int)prm.seed_pos[b];
@@ -106,34 +114,25 @@ __global__ void __launch_bounds__(NT, 1) fps_small_kernel(const GreedyParams prm
 #pragma unroll
     for (int u = 0; u < Q; u += 2) Upd<T>::pair(x, y, z, d, u, px, py, pz, nz);
     bits_t bv = A::bits(d[0]);
-    int bu = 0;
-    T bx = x[0], by = y[0], bz = z[0];
 #pragma unroll
-    for (int u = 1; u < Q; ++u) {
-      const bits_t v = A::bits(d[u]);
-      if (v > bv) {  // strict: the lowest slot (position) keeps a tie
-        bv = v;
-        bu = u;
-        bx = x[u];
-        by = y[u];
-        bz = z[u];
-      }
-    }
+    for (int u = 1; u < Q; ++u) bv = max(bv, A::bits(d[u]));
+    int bu = Q - 1;  // the lowest slot (position) holding the maximum
+#pragma unroll
+    for (int u = Q - 2; u >= 0; --u) bu = A::bits(d[u]) == bv ? u : bu;
     const uint32_t bi = (uint32_t)(tid * Q + bu);
     // warp argmax: max value, lowest position at that value (:98-107)
     const bits_t wv = A::warp_max(bv);
     const uint32_t wi = __reduce_min_sync(0xffffffffu, bv == wv ? bi : kNone);
-    if (bv == wv && bi == wi) rec[par][warp] = SmallRec<T>{wv, wi, bx, by, bz};
+    if (bv == wv && bi == wi) rec[par][warp] = SmallRec<T>{wv, wi};
     __syncthreads();
     // every warp: argmax over the NW warp records
     const bits_t rv = lane < NW ? rec[par][lane].v : A::kmin;
     const uint32_t ri = lane < NW ? rec[par][lane].pos : kNone;
     const bits_t gv = A::warp_max(rv);
     const uint32_t gi = __reduce_min_sync(0xffffffffu, rv == gv ? ri : kNone);
-    const int gl = __ffs(__ballot_sync(0xffffffffu, rv == gv && ri == gi)) - 1;
-    px = rec[par][gl].x;
-    py = rec[par][gl].y;
-    pz = rec[par][gl].z;
+    px = sx[gi];
+    py = sy[gi];
+    pz = sz[gi];
     // the winner leaves the candidate set (:169); its owner marks it
 #pragma unroll
     for (int u = 0; u < Q; ++u)
@@ -148,6 +147,7 @@ __global__ void __launch_bounds__(NT, 1) fps_small_kernel(const GreedyParams prm
 template <typename T, int NT, int Q>
 SmallInst make_sinst() {
   SmallInst k;
+  k.smem = (size_t)NT * Q * 3 * sizeof(T);
   k.dtype = sizeof(T) == 4 ? 0 : 1;
   k.nt = NT;
   k.q = Q;
@@ -157,9 +157,10 @@ SmallInst make_sinst() {
 
 const SmallInst* small_instances(int* count) {
   static const SmallInst insts[] = {
+      // float: 256 threads up to 8192 points (tools/sweep_small.py: the step
+      // time tracks nt * q, 256 threads edge out 512 / 1024 at equal capacity)
       make_sinst<float, 256, 2>(),   make_sinst<float, 256, 4>(),   make_sinst<float, 256, 8>(),
-      make_sinst<float, 512, 8>(),   make_sinst<float, 512, 12>(),  make_sinst<float, 512, 16>(),
-      make_sinst<float, 1024, 6>(),  make_sinst<float, 1024, 8>(),
+      make_sinst<float, 256, 16>(),  make_sinst<float, 256, 24>(),  make_sinst<float, 256, 32>(),
       make_sinst<double, 256, 2>(),  make_sinst<double, 256, 4>(),  make_sinst<double, 256, 8>(),
       make_sinst<double, 512, 8>(),  make_sinst<double, 512, 12>(), make_sinst<double, 512, 16>(),
   };
