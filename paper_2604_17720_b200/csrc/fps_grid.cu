@@ -1,35 +1,43 @@
-// K1g — multi-winner bucketed farthest-point sampling with a cell index.
+// K1g — multi-winner bucketed farthest-point sampling with a bucket-group index.
 //
-// Same contract and bit-exact results as K1 / K1b / K1m (restates
+// Same contract and bit-exact results as K1 / K1s / K1b / K1m (restates
 // run_kernel, reference pkg/src/flashfps/fps_core.py:110-175).
 //
-// K1m tests every bucket against every point selected in a round, although a
-// point can only change buckets within its influence radius.  K1g keeps the
-// bucket state in shared memory and indexes the buckets by a uniform grid of
-// cells (CSR: cell -> buckets whose box overlaps it), so a selected point p
-// only tests the buckets registered in the cells of the cube
-// [p - R, p + R]^3 where R^2 is an upper bound of every bucket's key:
-//   R^2 = the distance of the first winner of the previous round (keys only
-//   decrease, and that winner was the maximum then).
-// A bucket outside the cube has box_d2(p, box) >= R^2 >= its key, so the
-// exact test of K1b would not flag it either — the flagged set, and therefore
-// every result, is unchanged.  Buckets spanning more than kMaxCells cells are
-// kept in an "oversize" list tested against every point; while the cube is
-// large (early rounds) all buckets are tested.
+// A round selects up to KM consecutive greedy winners from one reduction: the
+// bucket keys (best point of each bucket) in argmax order c_1, c_2, ...; c_j is
+// the winner right after c_1..c_{j-1} if (a) d2(c_j, c_i) >= dist(c_j) and
+// (b) dist(c_j) > the second-best distance of c_i's bucket, for every i < j
+// (every other distance only decreases, every other key ranks below c_j).
 //
-// A round (J points selected by the previous round, J <= KM):
-//   A. flag: every selected point tests its candidate buckets exactly
-//      (box_d2 with the reference's rounded ops); hits OR the point's bit into
-//      the bucket's mask and append new buckets to the round list
+// The bucket table lives in shared memory (boxes, key value / position / xyz,
+// second best, the round's point mask).  Buckets are grouped by kGS = 32
+// consecutive rows (kd order keeps a group compact): each group has a union
+// box, its NCG best keys (candidates) and its (NCG+1)-th value.  A cloud's
+// buckets are split over a cluster of CL CTAs (bucket q -> rank q % CL).
+//
+// A round (J points accepted by the previous round, J <= KM):
+//   A. flag: warps per point test the group boxes against the group maxima
+//      (a group with box_d2 >= its max key holds no bucket the point can flag);
+//      | barrier | every hit (point, group) pair tests the group's 32 bucket
+//      boxes, one per lane, with the reference's rounded ops; a hit ORs the
+//      point's bit into the bucket's mask, the first one lists the bucket.
+//      While the search radius (the first winner's distance of the previous
+//      round, an upper bound of every key) is large, every bucket is tested.
 //   | barrier |
-//   B. re-evaluate the round list (balanced over warps, up to 4 buckets per
-//      batch): apply only the points in each bucket's mask -> new key (value,
-//      position, xyz) and second-best value into the bucket table
+//   B. re-evaluate the listed buckets (balanced over the warps, up to 4 in
+//      flight): only the points in each bucket's mask -> new key (value,
+//      position, xyz) and second best; the group is marked dirty
 //   | barrier |
-//   C. per-warp max over a contiguous slice of the table | barrier | every key
-//      >= tau, the KM-th largest warp max, joins the candidate list | barrier |
-//   D. every warp: top-KM of the list by rank, chain test (K1m), accepted
-//      prefix into its own copy (identical in all warps, no barrier)
+//   C. dirty groups: NCG best keys and the next value
+//   | barrier |
+//   R. R1: groups ranked by their maxima, the top-KM groups' candidates copied
+//      to a compact list | barrier | R2: ranks of those candidates
+//   | barrier |
+//   D. warp 0: the rank's top-KM records (the general path when a top group
+//      holds more top keys than candidates), pushed to every cluster peer with
+//      st.async + mbarrier, bitonic merge of the CL lists, chain test (a)/(b),
+//      accepted prefix published
+//   | barrier |
 #include <cuda_runtime.h>
 
 #include <cstdint>
