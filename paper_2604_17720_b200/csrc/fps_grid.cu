@@ -385,6 +385,37 @@ __global__ void __launch_bounds__(NT, 1) fps_grid_kernel(const BucketParams prm)
     }
   };
 
+  // bound of bucket q's next key once its key point c is selected: every
+  // other point x keeps min(dist(x), d2(x, c)) <= min(second best, the
+  // largest rounded d2 from c to the bucket's box) — per axis
+  // max(|RN(lo - c)|, |RN(hi - c)|) bounds |RN(x - c)| (RN is monotone), and
+  // the rounded squares and sums are monotone; condition (b) of the chain test
+  // uses this instead of the second best alone
+  auto tail_bound = [&](int q) -> bits_t {
+    const T* bq = box + (size_t)q * 6;
+    T g[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const T v = kx[q * 3 + c];
+      T lo, hi;
+      if constexpr (sizeof(T) == 4) {
+        lo = fabsf(__fsub_rn(bq[c], v));
+        hi = fabsf(__fsub_rn(bq[3 + c], v));
+      } else {
+        lo = fabs(__dsub_rn(bq[c], v));
+        hi = fabs(__dsub_rn(bq[3 + c], v));
+      }
+      g[c] = lo > hi ? lo : hi;
+    }
+    T fc;
+    if constexpr (sizeof(T) == 4)
+      fc = __fadd_rn(__fadd_rn(__fmul_rn(g[0], g[0]), __fmul_rn(g[1], g[1])), __fmul_rn(g[2], g[2]));
+    else
+      fc = __dadd_rn(__dadd_rn(__dmul_rn(g[0], g[0]), __dmul_rn(g[1], g[1])), __dmul_rn(g[2], g[2]));
+    const bits_t fb = A::bits(fc);
+    return k2[q] < fb ? k2[q] : fb;
+  };
+
   int k = 1;
   for (int round = 0; k < iters; ++round) {
     long long t0 = 0, t1 = 0, t2 = 0, t3 = 0;
@@ -783,7 +814,7 @@ __global__ void __launch_bounds__(NT, 1) fps_grid_kernel(const BucketParams prm)
       nc = nl;
       if (lane < nc) {
         const int q = top_w[0][lane];
-        cv = kv[q]; c2 = k2[q]; cpos = ki[q]; cq = q;
+        cv = kv[q]; c2 = tail_bound(q); cpos = ki[q]; cq = q;
         cx = kx[q * 3 + 0]; cy = kx[q * 3 + 1]; cz = kx[q * 3 + 2];
       }
     } else {
@@ -797,8 +828,8 @@ __global__ void __launch_bounds__(NT, 1) fps_grid_kernel(const BucketParams prm)
           const uint32_t bar = mapa(smem_u32(&xbar_s[par]), (uint32_t)peer);
           if (e < nl) {
             const int q = top_w[0][e];
-            R::send(dst, bar, kv[q], k2[q], ki[q], q * CL + rank, kx[q * 3 + 0], kx[q * 3 + 1],
-                    kx[q * 3 + 2], trunc ? 1u : 0u);
+            R::send(dst, bar, kv[q], tail_bound(q), ki[q], q * CL + rank, kx[q * 3 + 0],
+                    kx[q * 3 + 1], kx[q * 3 + 2], trunc ? 1u : 0u);
           } else {
             R::send(dst, bar, A::kmin, A::kmin, kNoIdx, -1, T(0), T(0), T(0), 0u);
           }
