@@ -311,11 +311,14 @@ def run_ours(args, rank: int, world: int, local_rank: int):
 
     def ramp(seconds=1.0):
         """Untimed load before the warm-up steps: a fresh box idles at low SM
-        clocks and needs a moment under load to reach its boost clock."""
+        clocks and needs a moment under load to reach its boost clock.
+        Time-bounded, so the ranks run different numbers of steps here: no
+        collective (the gather) inside, or the ranks' collectives mismatch."""
         t0 = time.perf_counter()
         while time.perf_counter() - t0 < seconds:
-            step(x, cfg_flash, True)
+            ffps.hierarchical_sample_batch(x, budgets, cfg_flash, 0, True)
             torch.cuda.synchronize()
+        barrier()
 
     def timed(cfg, cache, steps, warmup, timer=False):
         for _ in range(warmup):
