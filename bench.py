@@ -2,23 +2,28 @@
 """Benchmark of the FlashFPS hot path on B200 (BASELINE.json metric:
 "4-stage FPS clouds/sec & ms/cloud at N=200K; speedup vs exhaustive CUDA FPS").
 
-Workload (BASELINE.json configs[4], "C5" in SURVEY.md §8d): per rank a batch of
+Workload (BASELINE.json configs[4], "C5" in SURVEY.md §8d): a global batch of
 64 synthetic clouds of N=200,000 fp32 points (uniform unit cube, cloud b drawn
 from numpy default_rng(b), reference io.py:209-210), 4-stage budgets
-50000/12500/3125/781 (1/4 downsampling).  One step = hierarchical_sample of
-the whole batch with FPS-Prune p=0.75 + FPS-Cache (the FlashFPS pipeline:
-K1 greedy over the 50,000-point candidate prefix for 12,500 iterations, K2
-budget fill, layers 2-4 as prefix views) — plus, for N>1 ranks, the layer-1
-index gather.  The comparison arm is the same build's exhaustive 4-stage
-CUDA FPS (p=0, cache off: 200K->50K, then 50K->12.5K, 12.5K->3125,
-3125->781 restricted runs).
+50000/12500/3125/781 (1/4 downsampling), computed in binary64 like the
+reference (fps_core.py:74-83; the fp32 clouds upcast exactly, geometry.py:52-54;
+the kernels keep the coordinates as float and do every rounded operation in
+binary64: FFPS_F32_F64).  One step = hierarchical_sample of the batch with
+FPS-Prune p=0.75 + FPS-Cache (the FlashFPS pipeline: K0 bucket build + K1g
+greedy over the 50,000-point candidate prefix for 12,500 iterations, K2 budget
+fill, layers 2-4 as prefix views) — plus, for N>1 ranks, the layer-1 index
+gather.  The comparison arm is the same build's exhaustive 4-stage CUDA FPS
+(p=0, cache off: 200K->50K, then 50K->12.5K, 12.5K->3125, 3125->781
+restricted runs), also binary64.
 
 Arms:
   python bench.py [--gpus N --steps K --warmup W]        ours (one JSON line)
   python bench.py --impl reference ...                   the reference's CPU
-      algorithm (the oracle port, oracle/) on all host cores, same metric.
-Multi-GPU: torchrun, one rank per GPU, weak scaling (64 clouds per rank),
-timing = max over ranks of CUDA-event time.
+      algorithm in binary64 (the oracle port, oracle/) on all host cores.
+Multi-GPU: one rank per GPU (torchrun; `--gpus N` without torchrun re-launches
+itself under torch.distributed.run).  Strong scaling by default: the global
+batch of 64 clouds is split by cloud (sharded.shard_range); `--batch B` gives
+weak scaling (B clouds per rank).  Timing = max over ranks of CUDA-event time.
 """
 
 from __future__ import annotations
@@ -27,6 +32,7 @@ import argparse
 import json
 import math
 import os
+import socket
 import subprocess
 import sys
 import time
@@ -39,28 +45,34 @@ if ROOT not in sys.path:
 
 BUDGETS = {200_000: (50_000, 12_500, 3_125, 781), 300_000: (75_000, 18_750, 4_687, 1_171),
            100_000: (25_000, 6_250, 1_562, 390), 24_000: (6_000, 1_500, 375, 93)}
-BYTES_PER_UNIT_F32 = 20   # 12 B xyz read + 4 B dist read + 4 B dist write
-FLOPS_PER_UNIT = 9        # 3 sub + 3 mul + 2 add + 1 min
+BYTES_PER_UNIT = {"f32": 20, "f64": 40}  # xyz read + dist read + dist write
 METRIC = "4-stage FPS clouds/sec at N=200K (FPS-Prune p=0.75 + FPS-Cache)"
 
 
-def parse():
+def parse(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--batch", type=int, default=64, help="clouds per rank")
+    ap.add_argument("--global-batch", type=int, default=64,
+                    help="clouds per step over all ranks (strong scaling; BASELINE configs[4])")
+    ap.add_argument("--batch", type=int, default=None,
+                    help="clouds per rank (weak scaling; overrides --global-batch)")
     ap.add_argument("--n", type=int, default=200_000)
     ap.add_argument("--p", type=float, default=0.75)
+    ap.add_argument("--dtype", choices=["f64", "f32"], default="f64",
+                    help="arithmetic: f64 = the reference's binary64 (headline)")
     ap.add_argument("--cloud", choices=["uniform", "lidar"], default="uniform")
     ap.add_argument("--exh-steps", type=int, default=None,
                     help="timed steps of the exhaustive arm (default: --steps)")
     ap.add_argument("--no-exhaustive", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extras", action="store_true",
+                    help="skip the secondary measurements (f32 arm, divergence, quality)")
     ap.add_argument("--cpu-clouds", type=int, default=None,
                     help="clouds in the CPU sample (default: one per host core)")
-    return ap.parse_args()
+    return ap.parse_args(argv)
 
 
 # --------------------------------------------------------------------- inputs
@@ -191,6 +203,7 @@ SHARE_GPU = os.environ.get("FFPS_BENCH_SHARE_GPU") == "1"
 def gpu_index(local_rank: int) -> int:
     return 0 if SHARE_GPU else local_rank
 
+
 def peaks() -> dict:
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
@@ -224,12 +237,27 @@ def cpu_cores() -> int:
         return os.cpu_count() or 1
 
 
-def cpu_pipeline_sample(n: int, budgets, p: float, clouds: int, kind: str, threads: int):
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for ln in fh:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def cpu_pipeline_sample(n: int, budgets, p: float, clouds: int, kind: str, threads: int,
+                        dtype: str):
     """The reference algorithm on the host (oracle port, oracle/fps_oracle.c,
     restating fps_core.py:110-175 + fps_prune.py:68-111 + fps_cache.py:204-240),
-    one cloud per thread: returns (seconds, clouds)."""
+    one cloud per thread, binary64 on the upcast fp32 clouds (or binary32):
+    returns (seconds, clouds)."""
     from oracle import oracle
     xyz = make_clouds(kind, clouds, n, 10_000)
+    if dtype == "f64":
+        xyz = xyz.astype(np.float64)
     k = max(1, math.floor((1.0 - p) * budgets[0]))
     c = min(max(k, math.floor((1.0 - p) * n)), n)
     t0 = time.perf_counter()
@@ -245,6 +273,15 @@ def emit(obj):
     print(json.dumps(obj), flush=True)
 
 
+def shard(args, world: int, rank: int) -> tuple[int, int, int, str]:
+    """(first cloud, clouds on this rank, global batch, scaling)."""
+    from paper_2604_17720_b200.sharded import shard_range
+    if args.batch is not None:
+        return rank * args.batch, args.batch, args.batch * world, "weak"
+    lo, hi = shard_range(args.global_batch, world, rank)
+    return lo, hi - lo, args.global_batch, "strong"
+
+
 # ----------------------------------------------------------- reference arm
 def run_reference(args, rank: int, world: int):
     if rank != 0:
@@ -253,30 +290,53 @@ def run_reference(args, rank: int, world: int):
     cores = cpu_cores()
     clouds = args.cpu_clouds or cores
     for _ in range(min(args.warmup, 1)):
-        cpu_pipeline_sample(args.n, budgets, args.p, min(clouds, cores), args.cloud, cores)
+        cpu_pipeline_sample(args.n, budgets, args.p, min(clouds, cores), args.cloud, cores,
+                            args.dtype)
     times = []
     for _ in range(args.steps):
-        dt, cnt = cpu_pipeline_sample(args.n, budgets, args.p, clouds, args.cloud, cores)
+        dt, cnt = cpu_pipeline_sample(args.n, budgets, args.p, clouds, args.cloud, cores,
+                                      args.dtype)
         times.append(dt)
     sec = float(np.mean(times))
     val = clouds / sec
     sample = (f"{clouds} clouds of N={args.n} {args.cloud} per step, FPS-Prune p={args.p} "
-              f"+ FPS-Cache 4-stage {budgets}, one cloud per host thread")
+              f"+ FPS-Cache 4-stage {budgets}, binary{64 if args.dtype == 'f64' else 32}, "
+              f"one cloud per host thread on {cores} threads ({cpu_model()})")
+    _, _, gb, scaling = shard(args, world, 0)
     emit({"metric": METRIC, "impl": "reference", "value": val, "unit": "clouds/s",
           "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
           "ms_per_step": sec * 1e3, "ms_per_cloud": sec * 1e3 / clouds * cores,
-          "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-          "dtype": "f32", "data": "synthetic",
-          "config": {"workload": f"C5 FlashFPS 4-stage N={args.n}", "n": args.n,
-                     "budgets": list(budgets), "p": args.p, "cache": True,
-                     "cloud": args.cloud, "clouds_per_step": clouds},
+          "higher_is_better": True, "scaling": scaling, "vs_baseline": None,
+          "dtype": args.dtype, "data": "synthetic",
+          "config": {"workload": f"C5 FlashFPS 4-stage N={args.n} (BASELINE configs[4])",
+                     "n": args.n, "budgets": list(budgets), "p": args.p, "cache": True,
+                     "cloud": args.cloud, "global_batch": gb, "clouds_per_step": clouds},
           "cpu_baseline": {"value": val, "unit": "clouds/s", "cores": cores, "kind": "port",
-                           "sample": sample},
+                           "cpu": cpu_model(), "sample": sample},
           "e2e": {"value": val, "unit": "clouds/s", "h2d_bytes_per_step": 0,
                   "d2h_bytes_per_step": 0}})
 
 
 # ------------------------------------------------------------------ our arm
+def divergence(a: "torch.Tensor", b: "torch.Tensor", n: int) -> dict:
+    """Per-cloud comparison of two (B, k) index orders of the same clouds:
+    first differing position (-1: identical), positions that differ, and the
+    overlap of the two selected sets (|A & B| / k)."""
+    import torch
+    B, k = a.shape
+    diff = a != b
+    anyd = diff.any(1)
+    first = torch.where(anyd, diff.int().argmax(1), torch.full_like(anyd, -1, dtype=torch.int64))
+    mask = torch.zeros((B, n), dtype=torch.int8, device=a.device)
+    mask.scatter_(1, a, 1)
+    inter = mask.gather(1, b).sum(1)
+    return {"clouds": B, "k": k,
+            "identical_clouds": int((~anyd).sum()),
+            "first_divergence": [int(v) for v in first.cpu()],
+            "mismatched_positions": [int(v) for v in diff.sum(1).cpu()],
+            "set_overlap": [round(float(v) / k, 6) for v in inter.cpu()]}
+
+
 def run_ours(args, rank: int, world: int, local_rank: int):
     import torch
     import torch.distributed as dist
@@ -289,13 +349,13 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     dev = torch.device("cuda", gpu_index(local_rank))
     _native.load()
     budgets = BUDGETS[args.n]
-    B = args.batch
-    global_batch = B * world
+    first, B, global_batch, scaling = shard(args, world, rank)
+    prec = args.dtype                       # arithmetic of the headline
     cfg_flash = ffps.PruneConfig(p=args.p)
     cfg_exh = ffps.PruneConfig(p=0.0)
 
-    host = make_clouds(args.cloud, B, args.n, rank * B)
-    x = torch.from_numpy(host).to(dev)
+    host = make_clouds(args.cloud, B, args.n, first)
+    x = torch.from_numpy(host).to(dev)     # fp32 clouds resident in HBM
     pinned = torch.from_numpy(host).pin_memory()
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # > L2
 
@@ -303,8 +363,9 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         if world > 1:
             dist.barrier()
 
-    def step(xin, cfg, cache):
-        layers, total, _ = ffps.hierarchical_sample_batch(xin, budgets, cfg, 0, cache)
+    def step(cfg, cache, precision=prec):
+        layers, total, _ = ffps.hierarchical_sample_batch(x, budgets, cfg, 0, cache,
+                                                          precision=precision)
         if world > 1:
             gather_rows(layers[0].indices, global_batch)
         return layers, total
@@ -316,13 +377,13 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         collective (the gather) inside, or the ranks' collectives mismatch."""
         t0 = time.perf_counter()
         while time.perf_counter() - t0 < seconds:
-            ffps.hierarchical_sample_batch(x, budgets, cfg_flash, 0, True)
+            ffps.hierarchical_sample_batch(x, budgets, cfg_flash, 0, True, precision=prec)
             torch.cuda.synchronize()
         barrier()
 
-    def timed(cfg, cache, steps, warmup, timer=False):
+    def timed(cfg, cache, steps, warmup, timer=False, precision=prec):
         for _ in range(warmup):
-            step(x, cfg, cache)
+            step(cfg, cache, precision)
         torch.cuda.synchronize()
         barrier()
         ms, kern = [], []
@@ -334,12 +395,12 @@ def run_ours(args, rank: int, world: int, local_rank: int):
             if timer:
                 with _device.kernel_timer() as kt:
                     s.record()
-                    step(x, cfg, cache)
+                    step(cfg, cache, precision)
                     e.record()
             else:
                 kt = None
                 s.record()
-                step(x, cfg, cache)
+                step(cfg, cache, precision)
                 e.record()
             torch.cuda.synchronize()
             ms.append(s.elapsed_time(e))
@@ -362,12 +423,14 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     ms_step = tot_ms / args.steps
     value = global_batch / (ms_step / 1e3)
 
-    # end to end through the public host API: pinned host clouds in, host
-    # indices + selection distances out, every step
+    # end to end through the public host API: pinned fp32 host clouds in, host
+    # indices + binary64 selection distances out, every step
     out_i = torch.empty((B, budgets[0]), dtype=torch.int64).pin_memory()
-    out_s = torch.empty((B, budgets[0]), dtype=torch.float32).pin_memory()
+    out_s = torch.empty((B, budgets[0]),
+                        dtype=torch.float64 if prec == "f64" else torch.float32).pin_memory()
     for _ in range(args.warmup):
-        ffps.hierarchical_sample_host(pinned, budgets, cfg_flash, out=(out_i, out_s))
+        ffps.hierarchical_sample_host(pinned, budgets, cfg_flash, out=(out_i, out_s),
+                                      precision=prec)
     barrier()
     e2e_ms = []
     for _ in range(args.steps):
@@ -376,7 +439,8 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         s = torch.cuda.Event(enable_timing=True)
         e = torch.cuda.Event(enable_timing=True)
         s.record()
-        ffps.hierarchical_sample_host(pinned, budgets, cfg_flash, out=(out_i, out_s))
+        ffps.hierarchical_sample_host(pinned, budgets, cfg_flash, out=(out_i, out_s),
+                                      precision=prec)
         e.record()
         torch.cuda.synchronize()
         e2e_ms.append(s.elapsed_time(e))
@@ -386,9 +450,9 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         dist.all_reduce(e2e_tot, op=dist.ReduceOp.MAX)
     e2e_step = float(e2e_tot.item()) / args.steps
     e2e_val = global_batch / (e2e_step / 1e3)
-    c1_, _ = stage_units(args.n, budgets, args.p, True)[0]
-    h2d = B * c1_ * 3 * 4   # cache on: only the candidate prefix is read (fps_prune.py:92)
-    d2h = B * budgets[0] * (8 + 4)
+    c1_, k1_ = stage_units(args.n, budgets, args.p, True)[0]
+    h2d = B * c1_ * 3 * 4   # cache on: only the fp32 candidate prefix is read (fps_prune.py:92)
+    d2h = B * budgets[0] * (8 + out_s.element_size())
 
     # exhaustive 4-stage arm of the same build (the paper's "standard CUDA FPS")
     exh = None
@@ -410,112 +474,178 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         ex_step, ex_kern = arm(cfg_exh, False, "auto", ks)
         exh = {"value": global_batch / (ex_step / 1e3), "unit": "clouds/s",
                "ms_per_step": ex_step, "ms_per_cloud": ex_step / B, "steps": ks,
-               "schedule": "auto (" + _native.auto_schedule(args.n, B) + ")",
+               "dtype": prec, "schedule": "auto (" + _native.auto_schedule(args.n, B) + ")",
                "stage1_kernel_ms": float(np.mean([k[3] for k in ex_kern if k[1] == args.n])),
                "units_per_step": ex_units,
                "speedup_flash_vs_exhaustive": ex_step / ms_step}
         # the paper's baseline: standard FPS (every point every iteration, K1)
         sd_step, sd_kern = arm(cfg_exh, False, "stream", max(2, ks // 3))
         exh_std = {"value": global_batch / (sd_step / 1e3), "unit": "clouds/s",
-                   "ms_per_step": sd_step, "ms_per_cloud": sd_step / B,
+                   "ms_per_step": sd_step, "ms_per_cloud": sd_step / B, "dtype": prec,
                    "schedule": "stream (K1, standard exhaustive-update FPS)",
                    "stage1_kernel_ms": float(np.mean([k[3] for k in sd_kern if k[1] == args.n])),
                    "speedup_flash_vs_standard_exhaustive": sd_step / ms_step}
         fs_step, _ = arm(cfg_flash, True, "stream", max(2, ks // 3))
         flash_std = {"value": global_batch / (fs_step / 1e3), "unit": "clouds/s",
-                     "ms_per_step": fs_step, "schedule": "stream (K1)",
+                     "ms_per_step": fs_step, "schedule": "stream (K1)", "dtype": prec,
                      "speedup_flash_stream_vs_standard_exhaustive": sd_step / fs_step}
 
-    # matched sampling-quality metric (north star): covering radius of layer 1
-    # (metrics.py:45-52) for FlashFPS vs the exhaustive run, every cloud
-    quality = None
-    if not args.no_exhaustive:
-        fl_l, _, _ = ffps.hierarchical_sample_batch(x, budgets, cfg_flash, 0, True)
-        ex_l, _, _ = ffps.hierarchical_sample_batch(x, budgets, cfg_exh, 0, False)
-        torch.cuda.synchronize()
-        qs, qe = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        qs.record()
-        r_fl = ffps.coverage_radius_batch(x, fl_l[0].indices)
-        qe.record()
-        r_ex = ffps.coverage_radius_batch(x, ex_l[0].indices)
-        torch.cuda.synchronize()
-        ratio = (r_fl / r_ex).cpu().numpy()
-        quality = {"metric": "coverage radius of layer 1 (k-center objective, metrics.py:45-52)",
-                   "flash_mean": float(r_fl.mean()), "exhaustive_mean": float(r_ex.mean()),
-                   "ratio_median": float(np.median(ratio)), "ratio_max": float(ratio.max()),
-                   "coverage_kernel_ms_per_batch": qs.elapsed_time(qe), "clouds": B}
+    extras = {}
+    if not args.no_extras:
+        # the same pipeline in binary32 (secondary: not the reference's arithmetic)
+        f32_ms, _, _, _ = timed(cfg_flash, True, max(3, args.steps // 2), 1, precision="f32")
+        f32_step = f32_ms / max(3, args.steps // 2)
+        extras["f32"] = {"value": global_batch / (f32_step / 1e3), "unit": "clouds/s",
+                         "ms_per_step": f32_step,
+                         "note": "binary32 arithmetic: indices may differ from the reference "
+                                 "(see divergence)"}
+        # every divergence of binary32 from the reference's binary64, per cloud
+        fl64, _, _ = ffps.hierarchical_sample_batch(x, budgets, cfg_flash, 0, True,
+                                                    precision="f64")
+        fl32, _, _ = ffps.hierarchical_sample_batch(x, budgets, cfg_flash, 0, True,
+                                                    precision="f32")
+        div = {"flash_layer1_greedy": divergence(fl64[0].indices[:, :k1_],
+                                                 fl32[0].indices[:, :k1_], c1_)}
+        if not args.no_exhaustive:
+            ex64, _, _ = ffps.hierarchical_sample_batch(x, budgets, cfg_exh, 0, False,
+                                                        precision="f64")
+            ex32, _, _ = ffps.hierarchical_sample_batch(x, budgets, cfg_exh, 0, False,
+                                                        precision="f32")
+            div["exhaustive_layer1"] = divergence(ex64[0].indices, ex32[0].indices, args.n)
+        div["note"] = ("binary32 run vs the binary64 run (= the reference, bit for bit) on the "
+                       "same clouds; the headline is binary64, so its indices have no divergence")
+        extras["divergence_f32_vs_f64"] = div
+        # matched sampling-quality metric (north star): covering radius of layer 1
+        # (metrics.py:45-52) for FlashFPS vs the exhaustive run, every cloud
+        if not args.no_exhaustive:
+            torch.cuda.synchronize()
+            qs, qe = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            qs.record()
+            r_fl = ffps.coverage_radius_batch(x, fl64[0].indices, precision="f64")
+            qe.record()
+            r_ex = ffps.coverage_radius_batch(x, ex64[0].indices, precision="f64")
+            torch.cuda.synchronize()
+            ratio = (r_fl / r_ex).cpu().numpy()
+            extras["quality"] = {
+                "metric": "coverage radius of layer 1 (k-center objective, metrics.py:45-52)",
+                "flash_mean": float(r_fl.mean()), "exhaustive_mean": float(r_ex.mean()),
+                "ratio_median": float(np.median(ratio)), "ratio_max": float(ratio.max()),
+                "coverage_kernel_ms_per_batch": qs.elapsed_time(qe), "clouds": B}
 
-    # roofline of the dominant kernel (K1 on the flash stage)
-    c1, k1 = stage_units(args.n, budgets, args.p, True)[0]
-    units_launch = B * c1 * (k1 - 1)
-    kms = float(np.mean([k[3] for k in kern])) if kern else float("nan")
-    pk = peaks()
-    achieved = units_launch * BYTES_PER_UNIT_F32 / (kms / 1e3) / 1e9
-    sched_full = _native.auto_schedule(c1, B)   # e.g. "grid@2" = K1g, 2 CTAs per cloud
-    sched = sched_full.split("@")[0]
-    plan = {"schedule": sched, "schedule_auto": sched_full,
-            **_native.bucket_plan(_native.F32, c1)} \
-        if sched in ("bucket", "multi", "grid") else \
-        {"schedule": "stream", **_native.plan(_native.F32, c1, B)}
-    sm_mhz = clocks["sm_mhz"] or pk["sm_max_mhz"]
-    issue_ceiling = 148 * 128 * sm_mhz * 1e6 / 9.0   # ~9 FP32-pipe instr / unit
-    traffic = None
-    try:  # per-launch DRAM bytes of the same kernel from one `ncu --set full` capture
-        with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
-            tj = json.load(fh)
-        kname = {"bucket": "fps_bucket_kernel", "multi": "fps_multi_kernel",
-                 "grid": "fps_grid_kernel"}.get(plan["schedule"], "fps_greedy_kernel")
-        hit = [v for k_, v in tj.items() if kname in k_]
-        traffic = hit[0]["dram_bytes"] if hit else None
-    except (OSError, ValueError, KeyError):
-        traffic = None
-    roof = {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
-            "frac": achieved / pk["hbm_gbs"], "traffic": traffic,
-            "kernel": {"bucket": "fps_bucket_kernel (K1b)", "multi": "fps_multi_kernel (K1m)",
-                       "grid": "fps_grid_kernel (K1g)"}.get(plan["schedule"],
-                                                           "fps_greedy_kernel (K1)"),
-            "kernel_ms": kms,
-            "units_per_launch": units_launch, "bytes_per_unit": BYTES_PER_UNIT_F32,
-            "peak_src": pk["src"],
-            "note": ("algorithmic bytes of the standard streaming FPS (20 B per point-"
-                     "iteration = distance_evals) / time of one greedy call on the launching "
-                     "stream (CUDA events around ffps_run_kernel: for K1b/K1m/K1g that is "
-                     "the K0 bucket build plus the greedy kernel, so the greedy kernel alone "
-                     "is faster than kernel_ms); >1 because the state stays on chip / in L2 "
-                     "and the bucketed schedules skip provably unaffected buckets"),
-            "issue_bound": {"achieved_units_per_s": units_launch / (kms / 1e3),
-                            "ceiling_units_per_s": issue_ceiling,
-                            "frac": units_launch / (kms / 1e3) / issue_ceiling,
-                            "sm_mhz": sm_mhz},
-            "latency": {"iterations": k1, "ns_per_iteration": kms * 1e6 / k1},
-            "plan": plan}
+    roof = latency_roofline(args, x, budgets, cfg_flash, prec, kern, clocks, B)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cores = cpu_cores()
         clouds = args.cpu_clouds or cores
-        dt, cnt = cpu_pipeline_sample(args.n, budgets, args.p, clouds, args.cloud, cores)
+        dt, cnt = cpu_pipeline_sample(args.n, budgets, args.p, clouds, args.cloud, cores, prec)
         cpu = {"value": cnt / dt, "unit": "clouds/s", "cores": cores, "kind": "port",
+               "cpu": cpu_model(),
                "sample": f"{cnt} clouds of N={args.n} {args.cloud}, FPS-Prune p={args.p} + "
-                         f"FPS-Cache, one cloud per host thread, {dt:.1f} s wall"}
+                         f"FPS-Cache, binary{64 if prec == 'f64' else 32}, one cloud per host "
+                         f"thread, {dt:.1f} s wall"}
 
     if rank == 0:
         emit({"metric": METRIC, "value": value, "unit": "clouds/s", "n_gpus": world,
               "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
-              "ms_per_cloud": ms_step / B, "higher_is_better": True, "scaling": "weak",
-              "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+              "ms_per_cloud": ms_step / B, "higher_is_better": True, "scaling": scaling,
+              "vs_baseline": None, "dtype": prec, "data": "synthetic",
               "config": {"workload": f"C5 FlashFPS 4-stage N={args.n} (BASELINE configs[4])",
                          "n": args.n, "budgets": list(budgets), "p": args.p, "cache": True,
-                         "clouds_per_rank": B, "global_batch": global_batch,
-                         "cloud": args.cloud, "parallelism": f"shard-by-cloud x{world}",
+                         "global_batch": global_batch, "clouds_per_rank": B,
+                         "cloud": args.cloud, "input": "fp32 xyz",
+                         "arithmetic": "binary64 (FFPS_F32_F64)" if prec == "f64"
+                         else "binary32",
+                         "parallelism": f"shard-by-cloud x{world}",
                          "l2": "256 MiB flush write between timed steps"},
               "e2e": {"value": e2e_val, "unit": "clouds/s", "ms_per_step": e2e_step,
                       "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
               "gpu_launches": launches, "roofline": roof, "exhaustive": exh,
               "exhaustive_standard": exh_std, "flash_standard_schedule": flash_std,
-              "quality": quality,
+              **extras,
               "cpu_baseline": cpu, "clocks": clocks,
               "step_ms": [round(v, 4) for v in ms]})
+
+
+def latency_roofline(args, x, budgets, cfg_flash, prec, kern, clocks, B) -> dict:
+    """Roofline of the dominant kernel (K1g, the greedy stage of the step).
+
+    K1g never streams its state from HBM (the bucket table sits in shared
+    memory, the bucket SoA in L2), so bytes do not bound it: each greedy
+    round is a dependent chain (flag -> re-evaluate -> rank -> DSMEM exchange
+    -> chain test).  The bound is the latency of that chain.  Its floor is
+    measured live with the same kernel instance on a minimal table (one
+    bucket group per CTA, the same clusters per SM): peak = 1 / floor round
+    time.  achieved = the rounds of one C5 launch (kernel counters,
+    ffps_run_kernel_stats) / the greedy call's CUDA-event time (K0 bucket
+    build included, so frac is conservative)."""
+    import torch
+    import paper_2604_17720_b200 as ffps
+    from paper_2604_17720_b200 import _device, _native
+    c1, k1 = stage_units(args.n, budgets, args.p, True)[0]
+    sched = _native.auto_schedule(c1, B)
+    with _device.grid_stats() as gs:
+        ffps.hierarchical_sample_batch(x, budgets, cfg_flash, 0, True, precision=prec)
+    torch.cuda.synchronize()
+    st = [r for r in gs.records if r[1] == c1][0][3].double()
+    rounds = float(st[:, 0].mean())
+    cycles = float(st[:, 1].mean())
+    flagged = float(st[:, 2].mean())
+    # floor: minimal table, same instance family (KM, CL, bucket size 32)
+    nf = 1024 * (int(sched.split("@")[1]) if "@" in sched else 1)
+    floor_x = x[:, :nf].contiguous()
+    prev = _device.set_schedule(sched)
+    try:
+        with _device.grid_stats() as gf:
+            ffps.fps_batch(floor_x, nf // 2, precision=prec)
+            torch.cuda.synchronize()
+    finally:
+        _device.set_schedule(prev)
+    sf = gf.records[0][3].double()
+    f_rounds = float(sf[:, 0].mean())
+    f_cycles = float(sf[:, 1].mean())
+    floor_cpr = f_cycles / max(f_rounds, 1.0)
+    cpr = cycles / max(rounds, 1.0)
+    kms = float(np.mean([k[3] for k in kern if k[1] == c1])) if kern else float("nan")
+    sm_mhz = clocks.get("sm_mhz") or peaks()["sm_max_mhz"]
+    peak = sm_mhz * 1e6 / floor_cpr                  # rounds/s per cloud at the floor
+    achieved = rounds / (kms / 1e3)                  # rounds/s per cloud, event-timed
+    units = B * c1 * (k1 - 1)
+    return {"bound": "latency", "achieved": achieved, "peak": peak,
+            "unit": "greedy rounds/s per cloud", "frac": achieved / peak,
+            "traffic": dram_traffic("fps_grid_kernel"),
+            "kernel": "fps_grid_kernel (K1g) " + sched, "kernel_ms": kms,
+            "rounds_per_cloud": rounds, "winners_per_round": (k1 - 1) / max(rounds, 1.0),
+            "cycles_per_round": cpr, "floor_cycles_per_round": floor_cpr,
+            "frac_cycles": floor_cpr / cpr,
+            "floor": f"same kernel, {nf}-point clouds (one bucket group per CTA), "
+                     f"{nf // 2} iterations, {B} clouds: {f_rounds:.0f} rounds",
+            "buckets_reevaluated_per_round": flagged / max(rounds, 1.0),
+            "sm_mhz": sm_mhz,
+            "streaming_equivalent": {
+                "note": "NOT a roofline: the standard streaming FPS's algorithmic bytes "
+                        "(distance_evals x bytes/unit) over the greedy call's time",
+                "units_per_launch": units, "bytes_per_unit": BYTES_PER_UNIT[prec],
+                "gbs": units * BYTES_PER_UNIT[prec] / (kms / 1e3) / 1e9}}
+
+
+def dram_traffic(kname: str):
+    """Per-launch DRAM bytes of a kernel from one `ncu --set full` capture
+    (profiles/traffic.json), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
+            tj = json.load(fh)
+        hit = [v for k_, v in tj.items() if kname in k_ and "F32_F64" in k_] or \
+              [v for k_, v in tj.items() if kname in k_]
+        return hit[0]["dram_bytes"] if hit else None
+    except (OSError, ValueError, KeyError):
+        return None
+
+
+def free_port() -> int:
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
 
 
 def main():
@@ -523,6 +653,14 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        # --gpus is authoritative: one rank per GPU under torch.distributed.run
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+               f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+               f"--master-port={free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+        sys.exit(subprocess.call(cmd))
+    if world != args.gpus and not SHARE_GPU:
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}; launch one rank per GPU")
     if args.impl == "reference":
         run_reference(args, rank, world)
         return

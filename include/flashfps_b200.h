@@ -39,7 +39,15 @@ extern "C" {
 
 #define FFPS_ABI_VERSION 1
 
-enum ffps_dtype { FFPS_F32 = 0, FFPS_F64 = 1 };
+/* FFPS_F32      float coordinates, binary32 arithmetic, float sel_d2;
+ * FFPS_F64      double coordinates, binary64 arithmetic, double sel_d2 (the
+ *               reference's arithmetic, fps_core.py:74-83,124-126);
+ * FFPS_F32_F64  float coordinates, binary64 arithmetic, double sel_d2: the
+ *               reference run on fp32 clouds (PointCloud upcasts them exactly,
+ *               geometry.py:52-54), with coordinates stored and moved as
+ *               float.  Results are bit-identical to FFPS_F64 on the upcast
+ *               cloud. */
+enum ffps_dtype { FFPS_F32 = 0, FFPS_F64 = 1, FFPS_F32_F64 = 2 };
 
 enum ffps_status {
   FFPS_OK = 0,
@@ -103,6 +111,20 @@ enum ffps_algo { FFPS_ALGO_AUTO = 0, FFPS_ALGO_STREAM = 1, FFPS_ALGO_BUCKET = 2,
                  FFPS_ALGO_MULTI = 3, FFPS_ALGO_GRID = 4, FFPS_ALGO_SMALL = 5 };
 #define FFPS_ALGO_GRID_CL(c) (FFPS_ALGO_GRID | ((c) << 8))
 
+/* ffps_run_kernel_ex plus per-cloud counters of the multi-winner schedule:
+ * when `stats` (device, [batch][FFPS_STATS_WORDS] int64, caller-zeroed) is not
+ * NULL the GRID schedule writes, per cloud, the rounds of its greedy loop,
+ * the SM cycles the loop took on cluster rank 0, the buckets re-evaluated and
+ * the points loaded by those re-evaluations (summed over the cluster's CTAs);
+ * other schedules leave it untouched.  Used to report the latency roofline
+ * (cycles per round) next to the kernel time. */
+#define FFPS_STATS_WORDS 4
+int ffps_run_kernel_stats(int dtype, const void* xyz, int64_t batch,
+                          int64_t cloud_stride, int64_t n, int64_t iters,
+                          const int64_t* seed_pos, const int64_t* index_map,
+                          int64_t map_stride, int64_t* order, void* sel_d2,
+                          int64_t out_stride, void* stream, int algo, int64_t* stats);
+
 /* Host -> device copy of the candidate prefix xyz[b][0:n_prefix) of every
  * cloud (the only coordinates a cache-on FlashFPS run reads,
  * fps_prune.py:92) into a dense [batch][n_prefix][3] device buffer: one
@@ -164,6 +186,11 @@ int ffps_plan(int dtype, int64_t n, int64_t batch, int64_t* out);
 /* Bucketed-schedule configuration for n points: out[0]=threads/CTA,
  * out[1]=points per bucket, out[2]=buckets, out[3]=buckets owned per thread. */
 int ffps_bucket_plan(int dtype, int64_t n, int64_t* out);
+
+/* Hand the library's cached scratch memory (a private stream-ordered pool
+ * per device, up to 4 GiB kept mapped between calls) back to the driver;
+ * synchronises the current device. */
+int ffps_trim_scratch(void);
 
 /* Number of kernel launches the last successful call on this thread issued. */
 int64_t ffps_last_launch_count(void);

@@ -16,6 +16,7 @@ from .errors import KernelError
 _DTYPE_CODE = {torch.float32: _native.F32, torch.float64: _native.F64}
 _launches = 0
 _timers: list | None = None
+_stats: list | None = None
 _algo = "auto"
 
 
@@ -55,6 +56,25 @@ class kernel_timer:
         return [(b, n, it, s.elapsed_time(e)) for b, n, it, s, e in self.records]
 
 
+class grid_stats:
+    """Context manager that attaches a per-cloud counter block to every greedy
+    launch issued inside it (ffps_run_kernel_stats); ``records`` holds
+    (batch, n, iters, stats) with stats a (batch, 4) int64 device tensor:
+    rounds, loop cycles on cluster rank 0, re-evaluated buckets, points
+    loaded by the re-evaluations (grid schedule only; zeros otherwise)."""
+
+    def __enter__(self):
+        global _stats
+        self.records = []
+        _stats = self.records
+        return self
+
+    def __exit__(self, *exc):
+        global _stats
+        _stats = None
+        return False
+
+
 def launches() -> int:
     """Kernel launches issued by this process so far (K1 + K2)."""
     return _launches
@@ -76,11 +96,19 @@ def require_cuda(device=None) -> torch.device:
     return dev
 
 
-def dtype_code(t: torch.Tensor) -> int:
+def dtype_code(t: torch.Tensor, out: torch.Tensor | None = None) -> int:
+    """ABI dtype of coordinates ``t`` with results ``out`` (default: same
+    dtype): float32 coordinates with float64 results select FFPS_F32_F64,
+    binary64 arithmetic on float coordinates."""
     try:
-        return _DTYPE_CODE[t.dtype]
+        code = _DTYPE_CODE[t.dtype]
     except KeyError:
         raise TypeError(f"coordinates must be float32 or float64, got {t.dtype}") from None
+    if out is not None and out.dtype != t.dtype:
+        if t.dtype == torch.float32 and out.dtype == torch.float64:
+            return _native.F32_F64
+        raise TypeError(f"{t.dtype} coordinates cannot produce {out.dtype} distances")
+    return code
 
 
 def _stream_handle(stream) -> int:
@@ -98,7 +126,8 @@ def greedy(xyz: torch.Tensor, n: int, iters: int, seeds: torch.Tensor,
         return
     assert xyz.is_cuda and xyz.is_contiguous() and xyz.dim() == 3 and xyz.shape[2] == 3
     assert order.dtype == torch.int64 and order.stride(1) == 1 and sel.stride(1) == 1
-    assert sel.dtype == xyz.dtype and sel.stride(0) == order.stride(0)
+    assert sel.stride(0) == order.stride(0)
+    code = dtype_code(xyz, sel)
     assert seeds.dtype == torch.int64 and seeds.is_cuda and seeds.numel() == B
     map_ptr, map_stride = None, 0
     if index_map is not None:
@@ -110,10 +139,15 @@ def greedy(xyz: torch.Tensor, n: int, iters: int, seeds: torch.Tensor,
             ev0 = torch.cuda.Event(enable_timing=True)
             ev1 = torch.cuda.Event(enable_timing=True)
             ev0.record(strm)
-        _count(_native.run_kernel(dtype_code(xyz), xyz.data_ptr(), B, xyz.shape[1], n, iters,
+        st_ptr = None
+        if _stats is not None:
+            st_t = torch.zeros((B, _native.STATS_WORDS), dtype=torch.int64, device=xyz.device)
+            _stats.append((B, n, iters, st_t))
+            st_ptr = st_t.data_ptr()
+        _count(_native.run_kernel(code, xyz.data_ptr(), B, xyz.shape[1], n, iters,
                                   seeds.data_ptr(), map_ptr, map_stride, order.data_ptr(),
                                   sel.data_ptr(), order.stride(0), _stream_handle(stream),
-                                  _algo))
+                                  _algo, st_ptr))
         if _timers is not None:
             ev1.record(strm)
             _timers.append((B, n, iters, ev0, ev1))
@@ -159,8 +193,9 @@ def coverage(xyz: torch.Tensor, idx: torch.Tensor, out: torch.Tensor, stream=Non
     if B == 0:
         return
     assert xyz.is_cuda and xyz.is_contiguous() and idx.dtype == torch.int64
-    assert idx.stride(1) == 1 and out.dtype == xyz.dtype and out.is_contiguous()
+    assert idx.stride(1) == 1 and out.is_contiguous()
+    code = dtype_code(xyz, out)
     with torch.cuda.device(xyz.device):
-        _count(_native.coverage(dtype_code(xyz), xyz.data_ptr(), B, xyz.shape[1], xyz.shape[1],
+        _count(_native.coverage(code, xyz.data_ptr(), B, xyz.shape[1], xyz.shape[1],
                                 idx.data_ptr(), idx.stride(0), idx.shape[1], out.data_ptr(),
                                 _stream_handle(stream)))

@@ -24,6 +24,8 @@ if os.environ.get("FFPS_LIB_VARIANT"):
                             f"libflashfps_b200_{os.environ['FFPS_LIB_VARIANT']}.so")
 
 F32, F64 = 0, 1
+F32_F64 = 2   # float coordinates, binary64 arithmetic (FFPS_F32_F64)
+STATS_WORDS = 4
 ALGO = {"auto": 0, "stream": 1, "bucket": 2, "multi": 3, "grid": 4,
         # K1g with a fixed number of CTAs per cloud (FFPS_ALGO_GRID_CL(c))
         "grid@1": 4 | 1 << 8, "grid@2": 4 | 2 << 8, "grid@4": 4 | 4 << 8, "small": 5}
@@ -39,6 +41,9 @@ SIGNATURES = {
                                _vp, _i64, _vp]),
     "ffps_run_kernel_ex": (_int, [_int, _vp, _i64, _i64, _i64, _i64, _vp, _vp, _i64, _vp,
                                   _vp, _i64, _vp, _int]),
+    "ffps_run_kernel_stats": (_int, [_int, _vp, _i64, _i64, _i64, _i64, _vp, _vp, _i64, _vp,
+                                     _vp, _i64, _vp, _int, _vp]),
+    "ffps_trim_scratch": (_int, []),
     "ffps_fill_slice": (_int, [_int, _vp, _vp, _i64, _i64, _i64, _i64, _vp]),
     "ffps_fill_random": (_int, [_int, _vp, _vp, _i64, _i64, _i64, _i64, _i64, ctypes.c_uint64,
                                 ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64, _vp]),
@@ -82,13 +87,25 @@ def check(rc: int, what: str) -> None:
 
 
 def run_kernel(dtype, xyz, batch, cloud_stride, n, iters, seed_pos, index_map, map_stride,
-               order, sel_d2, out_stride, stream, algo: str = "auto") -> int:
+               order, sel_d2, out_stride, stream, algo: str = "auto", stats=None) -> int:
+    """``stats``: None or a device pointer to [batch][STATS_WORDS] int64 zeros
+    (per-cloud counters of the grid schedule, ffps_run_kernel_stats)."""
     lib = load()
-    check(lib.ffps_run_kernel_ex(dtype, xyz, batch, cloud_stride, n, iters, seed_pos,
-                                 index_map, map_stride, order, sel_d2, out_stride, stream,
-                                 ALGO[algo]),
-          "ffps_run_kernel")
+    if stats is None:
+        rc = lib.ffps_run_kernel_ex(dtype, xyz, batch, cloud_stride, n, iters, seed_pos,
+                                    index_map, map_stride, order, sel_d2, out_stride, stream,
+                                    ALGO[algo])
+    else:
+        rc = lib.ffps_run_kernel_stats(dtype, xyz, batch, cloud_stride, n, iters, seed_pos,
+                                       index_map, map_stride, order, sel_d2, out_stride, stream,
+                                       ALGO[algo], stats)
+    check(rc, "ffps_run_kernel")
     return int(lib.ffps_last_launch_count())
+
+
+def trim_scratch() -> None:
+    """Return the library's cached scratch memory to the driver."""
+    check(load().ffps_trim_scratch(), "ffps_trim_scratch")
 
 
 def fill_slice(dtype, order, sel_d2, batch, out_stride, k, m1, stream) -> int:

@@ -15,6 +15,13 @@ Validation raises the reference's exceptions before any device work; the
 stats are the reference's analytic counters for ONE cloud (every cloud of a
 batch has the same shape, so the same counters).  The single-cloud API in
 fps_core / fps_prune / fps_cache is this module with B = 1.
+
+``precision``: the arithmetic of the run.  None follows the coordinates
+(float32 -> binary32, float64 -> binary64).  "f64" on float32 coordinates
+runs the reference's binary64 arithmetic on them (PointCloud upcasts a float32
+cloud exactly, geometry.py:52-54) while the coordinates stay float32 in HBM,
+L2 and shared memory; selection distances come back as float64 and every
+result equals the float64 run on the upcast cloud, bit for bit.
 """
 
 from __future__ import annotations
@@ -88,6 +95,20 @@ def as_device_batch(xyz, device=None) -> torch.Tensor:
     return t.contiguous()
 
 
+def _out_dtype(x: torch.Tensor, precision) -> torch.dtype:
+    """dtype of the selection distances (= the arithmetic) for coordinates x."""
+    if precision is None:
+        return x.dtype
+    want = {"f64": torch.float64, "float64": torch.float64, torch.float64: torch.float64,
+            "f32": torch.float32, "float32": torch.float32, torch.float32: torch.float32}.get(
+                precision)
+    if want is None:
+        raise ValueError(f"precision must be None, 'f32' or 'f64'; got {precision!r}")
+    if want == torch.float32 and x.dtype == torch.float64:
+        raise ValueError("binary32 arithmetic on float64 coordinates would round the cloud")
+    return want
+
+
 def _shape(xyz) -> tuple[int, int]:
     """(B, N) of a (B, N, 3) or (N, 3) input without touching the device, so
     argument errors surface before any CUDA requirement."""
@@ -110,7 +131,8 @@ def _check_seeds(seeds: np.ndarray, n: int) -> None:
         raise SeedOutOfRange(f"seed index {s} not in [0, {n})")
 
 
-def fps_batch(xyz, m: int, seed_index=0, *, device=None) -> tuple[BatchSample, SamplerStats]:
+def fps_batch(xyz, m: int, seed_index=0, *, device=None,
+              precision=None) -> tuple[BatchSample, SamplerStats]:
     """Exhaustive FPS of every cloud (fps_core.py:185-196)."""
     B, n = _shape(xyz)
     if not 1 <= m <= n:
@@ -119,7 +141,7 @@ def fps_batch(xyz, m: int, seed_index=0, *, device=None) -> tuple[BatchSample, S
     _check_seeds(seeds, n)
     x = as_device_batch(xyz, device)
     order = torch.empty((B, m), dtype=torch.int64, device=x.device)
-    sel = torch.empty((B, m), dtype=x.dtype, device=x.device)
+    sel = torch.empty((B, m), dtype=_out_dtype(x, precision), device=x.device)
     _device.greedy(x, n, m, _device.seeds_tensor(seeds, B, x.device), order, sel)
     return (BatchSample(order, sel, m),
             SamplerStats(distance_evals=n * (m - 1), iterations=m, candidates=n))
@@ -141,7 +163,7 @@ def _fps_prune_checks(B: int, n: int, m1: int, cfg: PruneConfig, seeds: np.ndarr
 
 
 def _fps_prune_device(x: torch.Tensor, m1: int, cfg: PruneConfig, seeds: np.ndarray,
-                      n: int | None = None):
+                      n: int | None = None, precision=None):
     """``x`` holds at least the candidate prefix of every cloud; ``n`` is the
     logical cloud size (x.shape[1] when the whole cloud is on the device)."""
     B = x.shape[0]
@@ -149,7 +171,7 @@ def _fps_prune_device(x: torch.Tensor, m1: int, cfg: PruneConfig, seeds: np.ndar
     k, c = _fps_prune_checks(B, n, m1, cfg, seeds)
     assert x.shape[1] >= c
     order = torch.empty((B, m1), dtype=torch.int64, device=x.device)
-    sel = torch.empty((B, m1), dtype=x.dtype, device=x.device)
+    sel = torch.empty((B, m1), dtype=_out_dtype(x, precision), device=x.device)
     # candidates are the store prefix [0, c): kernel positions == original indices
     _device.greedy(x, c, k, _device.seeds_tensor(seeds, B, x.device), order, sel)
     if m1 > k:
@@ -162,20 +184,29 @@ def _fps_prune_device(x: torch.Tensor, m1: int, cfg: PruneConfig, seeds: np.ndar
 
 
 def fps_prune_batch(xyz, m1: int, cfg: PruneConfig, seed_index=0, *,
-                    device=None) -> tuple[BatchSample, SamplerStats]:
+                    device=None, precision=None) -> tuple[BatchSample, SamplerStats]:
     """FPS-Prune for every cloud (fps_prune.py:68-111)."""
     B, n = _shape(xyz)
     seeds = _seed_array(seed_index, B)
     _fps_prune_checks(B, n, m1, cfg, seeds)
-    return _fps_prune_device(as_device_batch(xyz, device), m1, cfg, seeds)
+    return _fps_prune_device(as_device_batch(xyz, device), m1, cfg, seeds,
+                             precision=precision)
 
 
 def run_restricted_batch(xyz, index_map, m: int, seed_pos=0, *,
-                         device=None) -> tuple[BatchSample, SamplerStats]:
+                         device=None, precision=None) -> tuple[BatchSample, SamplerStats]:
     """Exact FPS over xyz[b][index_map[b]] in map order, reported in original
-    indices (fps_cache.py:189-201); the gather happens inside the kernel."""
-    B, _ = _shape(xyz)
-    nm = int(np.shape(index_map)[-1])
+    indices (fps_cache.py:189-201); the gather happens inside the kernel.
+
+    ``index_map`` is (B, M) or (M,) (the same map for every cloud).  As the
+    reference's ``points[index_map]`` (fps_cache.py:195): negative entries
+    count from the end of the cloud, entries outside [-N, N) raise IndexError —
+    checked before any kernel reads the cloud."""
+    B, N = _shape(xyz)
+    shp = tuple(np.shape(index_map))
+    if len(shp) not in (1, 2) or (len(shp) == 2 and shp[0] != B):
+        raise ValueError(f"index_map must have shape ({B}, M) or (M,); got {shp}")
+    nm = int(shp[-1])
     if not 1 <= m <= nm:
         raise BudgetOutOfRange(f"m={m} not in [1, {nm}]")
     seeds = _seed_array(seed_pos, B)
@@ -183,13 +214,26 @@ def run_restricted_batch(xyz, index_map, m: int, seed_pos=0, *,
     x = as_device_batch(xyz, device)
     imap = index_map if isinstance(index_map, torch.Tensor) else \
         torch.from_numpy(np.ascontiguousarray(np.asarray(index_map, dtype=np.int64)))
-    if imap.dim() == 1:
-        imap = imap.unsqueeze(0)
+    if imap.dtype.is_floating_point or imap.dtype == torch.bool:
+        raise IndexError("index_map must hold integers")
     imap = imap.to(x.device, torch.int64)
-    if imap.stride(-1) != 1:
-        imap = imap.contiguous()
+    if imap.dim() == 1:
+        imap = imap.unsqueeze(0).expand(B, nm)
+    lo, hi = torch.aminmax(imap)
+    if int(lo) < -N or int(hi) >= N:
+        bad = int(lo) if int(lo) < -N else int(hi)
+        raise IndexError(f"index {bad} is out of bounds for a cloud of {N} points")
+    if int(lo) < 0:
+        imap = torch.where(imap < 0, imap + N, imap)
+    return _run_restricted_device(x, imap.contiguous(), m, seeds, precision)
+
+
+def _run_restricted_device(x: torch.Tensor, imap: torch.Tensor, m: int, seeds: np.ndarray,
+                           precision=None) -> tuple[BatchSample, SamplerStats]:
+    """run_restricted on a validated (B, M) int64 device map in [0, N)."""
+    B, nm = x.shape[0], imap.shape[1]
     order = torch.empty((B, m), dtype=torch.int64, device=x.device)
-    sel = torch.empty((B, m), dtype=x.dtype, device=x.device)
+    sel = torch.empty((B, m), dtype=_out_dtype(x, precision), device=x.device)
     _device.greedy(x, nm, m, _device.seeds_tensor(seeds, B, x.device), order, sel,
                    index_map=imap)
     return (BatchSample(order, sel, m),
@@ -204,7 +248,7 @@ def _budgets(budgets) -> tuple[int, ...]:
 
 
 def hierarchical_sample_batch(xyz, budgets: Sequence[int], cfg: PruneConfig, seed_index=0,
-                              cache_enabled: bool = True, *, device=None):
+                              cache_enabled: bool = True, *, device=None, precision=None):
     """Every layer of the budget pyramid for every cloud
     (fps_cache.py:204-240).  Returns (layers, total, per_layer): with the cache
     on, layers 2..L are prefix views of layer 1 (zero distance evaluations);
@@ -217,7 +261,7 @@ def hierarchical_sample_batch(xyz, budgets: Sequence[int], cfg: PruneConfig, see
     seeds = _seed_array(seed_index, B)
     _fps_prune_checks(B, n, b[0], cfg, seeds)
     x = as_device_batch(xyz, device)
-    layer1, stats1 = _fps_prune_device(x, b[0], cfg, seeds)
+    layer1, stats1 = _fps_prune_device(x, b[0], cfg, seeds, precision=precision)
     layers, per_layer = [layer1], [stats1]
     if cache_enabled:
         stats1.cache_bytes = cache_footprint_bytes(b[0])
@@ -226,8 +270,9 @@ def hierarchical_sample_batch(xyz, budgets: Sequence[int], cfg: PruneConfig, see
                                       min(layer1.fill_boundary, m)))
             per_layer.append(SamplerStats())
     else:
-        for m in b[1:]:
-            s, st = run_restricted_batch(x, layers[-1].indices, m, 0)
+        zero = np.zeros(B, dtype=np.int64)
+        for m in b[1:]:  # the previous layer's indices are valid by construction
+            s, st = _run_restricted_device(x, layers[-1].indices, m, zero, precision)
             layers.append(s)
             per_layer.append(st)
     total = SamplerStats(
@@ -251,7 +296,7 @@ def _side_streams(dev: torch.device, n: int) -> list:
 
 def hierarchical_sample_host(points, budgets: Sequence[int], cfg: PruneConfig, seed_index=0,
                              cache_enabled: bool = True, *, device=None, out=None,
-                             chunks: int = 4):
+                             chunks: int = 4, precision=None):
     """End-to-end call from HOST buffers: ``points`` (B, N, 3) float32/float64
     numpy array or (preferably pinned) CPU tensor.  Copies the clouds to the
     device, runs the pipeline, copies every layer's indices and selection
@@ -276,7 +321,8 @@ def hierarchical_sample_host(points, budgets: Sequence[int], cfg: PruneConfig, s
         np.ascontiguousarray(points))
     if not cache_enabled:
         x = host.to(dev, non_blocking=host.is_pinned())
-        layers, total, _ = hierarchical_sample_batch(x, b, cfg, seed_index, False)
+        layers, total, _ = hierarchical_sample_batch(x, b, cfg, seed_index, False,
+                                                     precision=precision)
         res = [(s.indices.to("cpu", non_blocking=True),
                 s.selection_dist2.to("cpu", non_blocking=True), s.fill_boundary)
                for s in layers]
@@ -287,7 +333,7 @@ def hierarchical_sample_host(points, budgets: Sequence[int], cfg: PruneConfig, s
         hi, hs = out
     else:
         hi = torch.empty((B, b[0]), dtype=torch.int64, pin_memory=pinned)
-        hs = torch.empty((B, b[0]), dtype=host.dtype, pin_memory=pinned)
+        hs = torch.empty((B, b[0]), dtype=_out_dtype(host, precision), pin_memory=pinned)
     nch = max(1, min(chunks, B))
     bounds = [B * i // nch for i in range(nch + 1)]
     # one schedule for the whole batch (AUTO would otherwise decide per chunk)
@@ -316,7 +362,8 @@ def hierarchical_sample_host(points, budgets: Sequence[int], cfg: PruneConfig, s
                         st.synchronize()  # pageable source: the copy is staged, keep it alive
                 else:
                     x = host[lo:up, :c].to(dev, non_blocking=pinned)
-                l1, stats1 = _fps_prune_device(x, b[0], cfg, seeds[lo:up], n=N)
+                l1, stats1 = _fps_prune_device(x, b[0], cfg, seeds[lo:up], n=N,
+                                               precision=precision)
                 hi[lo:up].copy_(l1.indices, non_blocking=pinned)
                 hs[lo:up].copy_(l1.selection_dist2, non_blocking=pinned)
         for st in streams:

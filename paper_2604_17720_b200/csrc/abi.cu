@@ -45,23 +45,46 @@ std::map<int, DeviceInfo> g_dev;
 std::map<std::tuple<int, const void*, int>, int> g_occ;  // (device, fn, C) -> max active clusters
 std::map<std::pair<int, const void*>, bool> g_attr_done;
 
+std::map<int, cudaMemPool_t> g_pool;  // library scratch pool per device
+
+// Scratch (spill buffers, K0 buckets, widened clouds) comes from a private
+// stream-ordered pool per device, so the caller's default pool keeps its own
+// attributes.  The pool keeps up to kKeepBytes mapped across synchronisations
+// (a release threshold of 0 would hand the memory back at every sync and the
+// next call would re-map it on the host: tens of ms for ~100 MB); beyond that
+// it releases, and ffps_trim_scratch() hands everything back.
+constexpr uint64_t kKeepBytes = 4ull << 30;
+
+cudaError_t pool_for(int dev, cudaMemPool_t* out) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  auto it = g_pool.find(dev);
+  if (it != g_pool.end()) {
+    *out = it->second;
+    return cudaSuccess;
+  }
+  cudaMemPoolProps props;
+  memset(&props, 0, sizeof props);
+  props.allocType = cudaMemAllocationTypePinned;
+  props.location.type = cudaMemLocationTypeDevice;
+  props.location.id = dev;
+  cudaMemPool_t pool;
+  cudaError_t e = cudaMemPoolCreate(&pool, &props);
+  if (e != cudaSuccess) return e;
+  uint64_t keep = kKeepBytes;
+  cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  // no hidden cross-stream waits: chunks of one batch on side streams must
+  // not be serialised by the pool reusing another stream's freed block
+  int no = 0;
+  cudaMemPoolSetAttribute(pool, cudaMemPoolReuseAllowInternalDependencies, &no);
+  cudaGetLastError();
+  g_pool[dev] = pool;
+  *out = pool;
+  return cudaSuccess;
+}
+
 DeviceInfo device_info_nolock(int dev) {
   auto it = g_dev.find(dev);
   if (it != g_dev.end()) return it->second;
-  // Scratch (spill buffers, K0 buckets) comes from the device's default
-  // stream-ordered pool.  Its release threshold defaults to 0, i.e. the pool
-  // hands memory back at every synchronisation and the next call re-maps it
-  // on the host (tens of ms for ~100 MB); keep it.
-  cudaMemPool_t pool;
-  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-    uint64_t keep = UINT64_MAX;
-    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
-    // no hidden cross-stream waits: chunks of one batch on side streams must
-    // not be serialised by the pool reusing another stream's freed block
-    int no = 0;
-    cudaMemPoolSetAttribute(pool, cudaMemPoolReuseAllowInternalDependencies, &no);
-  }
-  cudaGetLastError();
   DeviceInfo d;
   int v = 0;
   cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
@@ -220,7 +243,35 @@ bool make_plan(int dev, int dtype, int64_t n, int64_t batch, Plan* out) {
 
 }  // namespace
 
+namespace ffps {
+
+cudaError_t scratch_alloc(void** p, size_t bytes, cudaStream_t st) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  cudaMemPool_t pool;
+  e = pool_for(dev, &pool);
+  if (e != cudaSuccess) return e;
+  return cudaMallocFromPoolAsync(p, bytes, pool, st);
+}
+
+cudaError_t scratch_free(void* p, cudaStream_t st) { return cudaFreeAsync(p, st); }
+
+}  // namespace ffps
+
 extern "C" {
+
+int ffps_trim_scratch(void) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+  cudaMemPool_t pool;
+  e = pool_for(dev, &pool);
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e == cudaSuccess) e = cudaMemPoolTrimTo(pool, 0);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMemPoolTrimTo");
+  return FFPS_OK;
+}
 
 int ffps_abi_version(void) { return FFPS_ABI_VERSION; }
 
@@ -229,8 +280,10 @@ const char* ffps_last_error(void) { return g_last_error.c_str(); }
 int64_t ffps_last_launch_count(void) { return g_last_launches; }
 
 int ffps_plan(int dtype, int64_t n, int64_t batch, int64_t* out) {
-  if ((dtype != FFPS_F32 && dtype != FFPS_F64) || n < 1 || batch < 1 || !out)
+  if ((dtype != FFPS_F32 && dtype != FFPS_F64 && dtype != FFPS_F32_F64) || n < 1 || batch < 1 ||
+      !out)
     return fail(FFPS_EINVAL, "ffps_plan: bad arguments");
+  if (dtype == FFPS_F32_F64) dtype = FFPS_F64;  // K1 runs on the widened cloud
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
@@ -312,11 +365,12 @@ int run_bucketed(int dtype, const void* xyz, int64_t batch, int64_t cloud_stride
   // + TX, TY, TZ, TO for the second sort level of K0
   const size_t per_cloud = (size_t)nslots * (7 * esz + 8) + (size_t)bp.nbuckets * 6 * esz;
   unsigned char* scratch = nullptr;
-  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&scratch),
+  cudaError_t e = ffps::scratch_alloc(reinterpret_cast<void**>(&scratch),
                                   per_cloud * (size_t)batch + 512, st);
-  if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync(buckets)");
+  if (e != cudaSuccess) return cuda_fail(e, "scratch_alloc(buckets)");
   const size_t arr = (size_t)nslots * esz * (size_t)batch;
   ffps::BucketBuildParams bb;
+  bb.d_wide = 0;
   bb.xyz = xyz;
   bb.cloud_stride = cloud_stride;
   bb.index_map = index_map;
@@ -345,7 +399,7 @@ int run_bucketed(int dtype, const void* xyz, int64_t batch, int64_t cloud_stride
   }
   e = ffps::launch_bucket_build(dtype, bb, batch, st);
   if (e != cudaSuccess) {
-    cudaFreeAsync(scratch, st);
+    ffps::scratch_free(scratch, st);
     return cuda_fail(e, "bucket_build_kernel launch");
   }
   ffps::BucketParams prm;
@@ -369,6 +423,7 @@ int run_bucketed(int dtype, const void* xyz, int64_t batch, int64_t cloud_stride
   prm.neg_zero = -0.0f;
   prm.trace = nullptr;
   prm.trace_iters = 0;
+  prm.stats = nullptr;
   // FFPS_TRACE_BUCKET=<device pointer>,<iterations>: phase trace of CTA 0
   if (const char* tr = getenv(multi ? "FFPS_TRACE_MULTI" : "FFPS_TRACE_BUCKET")) {
     unsigned long long ptr = 0;
@@ -381,12 +436,12 @@ int run_bucketed(int dtype, const void* xyz, int64_t batch, int64_t cloud_stride
   void* args[] = {&prm};
   e = cudaLaunchKernel(k.fn, dim3((unsigned)batch), dim3(k.nt), args, 0, st);
   if (e != cudaSuccess) {
-    cudaFreeAsync(scratch, st);
+    ffps::scratch_free(scratch, st);
     return cuda_fail(e, "fps_bucket_kernel launch");
   }
   g_last_launches = 1 + ffps::bucket_build_launches(bb);
-  e = cudaFreeAsync(scratch, st);
-  if (e != cudaSuccess) return cuda_fail(e, "cudaFreeAsync(buckets)");
+  e = ffps::scratch_free(scratch, st);
+  if (e != cudaSuccess) return cuda_fail(e, "scratch_free(buckets)");
   return FFPS_OK;
 }
 
@@ -396,7 +451,7 @@ int grid_cluster(int algo, int64_t batch, int sms, int64_t n);
 int run_grid(int dtype, const void* xyz, int64_t batch, int64_t cloud_stride, int64_t n,
              int64_t iters, const int64_t* seed_pos, const int64_t* index_map, int64_t map_stride,
              int64_t* order, void* sel_d2, int64_t out_stride, cudaStream_t st, int dev,
-             int algo) {
+             int algo, int64_t* stats) {
   const DeviceInfo di = device_info(dev);
   int cnt = 0;
   const ffps::GridInst* insts = ffps::grid_instances(&cnt);
@@ -430,14 +485,18 @@ int run_grid(int dtype, const void* xyz, int64_t batch, int64_t cloud_stride, in
   if (!pick) return fail(FFPS_EUNSUPPORTED, "no grid configuration for n=%lld", (long long)n);
   const int64_t bs = 32 * pick->ppl;
   const int64_t nslots = nb * bs;
-  const size_t esz = pick->esz;
-  const size_t per_cloud = (size_t)nslots * (7 * esz + 8) + (size_t)nb * 6 * esz;
+  const size_t esz = pick->esz;                     // stored coordinate
+  const size_t desz = dtype == FFPS_F32 ? 4 : 8;    // running distance (arithmetic type)
+  // X, Y, Z, D, boxes, O + the K0 scratch TX, TY, TZ, TO
+  const size_t per_cloud = (size_t)nslots * (6 * esz + desz + 8) + (size_t)nb * 6 * esz;
   unsigned char* scratch = nullptr;
-  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&scratch),
+  cudaError_t e = ffps::scratch_alloc(reinterpret_cast<void**>(&scratch),
                                   per_cloud * (size_t)batch + 512, st);
-  if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync(grid)");
+  if (e != cudaSuccess) return cuda_fail(e, "scratch_alloc(grid)");
   const size_t arr = (size_t)nslots * esz * (size_t)batch;
+  const size_t darr = (size_t)nslots * desz * (size_t)batch;
   ffps::BucketBuildParams bb;
+  bb.d_wide = dtype == FFPS_F32_F64 ? 1 : 0;
   bb.xyz = xyz;
   bb.cloud_stride = cloud_stride;
   bb.index_map = index_map;
@@ -447,8 +506,8 @@ int run_grid(int dtype, const void* xyz, int64_t batch, int64_t cloud_stride, in
   bb.Y = scratch + arr;
   bb.Z = scratch + 2 * arr;
   bb.D = scratch + 3 * arr;
-  bb.BB = scratch + 4 * arr;
-  bb.O = reinterpret_cast<int32_t*>(scratch + 4 * arr + box_bytes(nb, esz, batch));
+  bb.BB = scratch + 3 * arr + darr;
+  bb.O = reinterpret_cast<int32_t*>(scratch + 3 * arr + darr + box_bytes(nb, esz, batch));
   bb.nslots = nslots;
   bb.nbuckets = nb;
   bb.bs = bs;
@@ -459,9 +518,10 @@ int run_grid(int dtype, const void* xyz, int64_t batch, int64_t cloud_stride, in
     bb.TZ = t + 2 * arr;
     bb.TO = reinterpret_cast<int32_t*>(t + 3 * arr);
   }
-  e = ffps::launch_bucket_build(dtype, bb, batch, st);
+  // K0 sorts float coordinates under FFPS_F32_F64 (D written as double)
+  e = ffps::launch_bucket_build(dtype == FFPS_F32_F64 ? FFPS_F32 : dtype, bb, batch, st);
   if (e != cudaSuccess) {
-    cudaFreeAsync(scratch, st);
+    ffps::scratch_free(scratch, st);
     return cuda_fail(e, "bucket_build_kernel launch");
   }
   ffps::BucketParams prm;
@@ -473,6 +533,7 @@ int run_grid(int dtype, const void* xyz, int64_t batch, int64_t cloud_stride, in
   prm.BB = bb.BB;
   prm.nslots = nslots;
   prm.nbuckets = nb;
+  prm.stats = reinterpret_cast<long long*>(stats);
   prm.xyz = xyz;
   prm.cloud_stride = cloud_stride;
   prm.index_map = index_map;
@@ -503,7 +564,7 @@ int run_grid(int dtype, const void* xyz, int64_t batch, int64_t cloud_stride, in
         e = cudaFuncSetAttribute(pick->fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)(device_info_nolock(dev).smem_optin - fa.sharedSizeBytes));
       if (e != cudaSuccess) {
-        cudaFreeAsync(scratch, st);
+        ffps::scratch_free(scratch, st);
         return cuda_fail(e, "cudaFuncSetAttribute(grid)");
       }
       g_attr_done[key] = true;
@@ -526,12 +587,12 @@ int run_grid(int dtype, const void* xyz, int64_t batch, int64_t cloud_stride, in
     e = cudaLaunchKernelExC(&lc, pick->fn, args);
   }
   if (e != cudaSuccess) {
-    cudaFreeAsync(scratch, st);
+    ffps::scratch_free(scratch, st);
     return cuda_fail(e, "fps_grid_kernel launch");
   }
   g_last_launches = 1 + ffps::bucket_build_launches(bb);
-  e = cudaFreeAsync(scratch, st);
-  if (e != cudaSuccess) return cuda_fail(e, "cudaFreeAsync(grid)");
+  e = ffps::scratch_free(scratch, st);
+  if (e != cudaSuccess) return cuda_fail(e, "scratch_free(grid)");
   return FFPS_OK;
 }
 
@@ -618,8 +679,8 @@ int run_streaming(int dtype, const void* xyz, int64_t batch, int64_t cloud_strid
   if (plan.G > 0) {
     const size_t bytes =
         ffps::spill_bytes_per_cta(dtype, k.nt, plan.G) * (size_t)plan.C * (size_t)batch;
-    e = cudaMallocAsync(&prm.spill, bytes, st);
-    if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync(spill)");
+    e = ffps::scratch_alloc(&prm.spill, bytes, st);
+    if (e != cudaSuccess) return cuda_fail(e, "scratch_alloc(spill)");
   }
 
   // Clusters of a batch beyond the device's resident capacity simply queue;
@@ -640,13 +701,13 @@ int run_streaming(int dtype, const void* xyz, int64_t batch, int64_t cloud_strid
   void* args[] = {&prm};
   e = cudaLaunchKernelExC(&cfg, k.fn, args);
   if (e != cudaSuccess) {
-    if (prm.spill) cudaFreeAsync(prm.spill, st);
+    if (prm.spill) ffps::scratch_free(prm.spill, st);
     return cuda_fail(e, "fps_greedy_kernel launch");
   }
   g_last_launches = 1;
   if (prm.spill) {
-    e = cudaFreeAsync(prm.spill, st);
-    if (e != cudaSuccess) return cuda_fail(e, "cudaFreeAsync(spill)");
+    e = ffps::scratch_free(prm.spill, st);
+    if (e != cudaSuccess) return cuda_fail(e, "scratch_free(spill)");
   }
   return FFPS_OK;
 }
@@ -707,8 +768,9 @@ int grid_cluster(int algo, int64_t batch, int sms, int64_t n) {
 extern "C" {
 
 int ffps_bucket_plan(int dtype, int64_t n, int64_t* out) {
-  if ((dtype != FFPS_F32 && dtype != FFPS_F64) || n < 1 || !out)
+  if ((dtype != FFPS_F32 && dtype != FFPS_F64 && dtype != FFPS_F32_F64) || n < 1 || !out)
     return fail(FFPS_EINVAL, "ffps_bucket_plan: bad arguments");
+  if (dtype == FFPS_F32_F64) dtype = FFPS_F64;  // K1b runs on the widened cloud
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
@@ -725,12 +787,12 @@ int ffps_bucket_plan(int dtype, int64_t n, int64_t* out) {
 int ffps_h2d_prefix(void* dst, const void* src_host, int64_t batch, int64_t n_prefix,
                     int64_t cloud_stride, int dtype, void* stream) {
   g_last_launches = 0;
-  if ((dtype != FFPS_F32 && dtype != FFPS_F64) || batch < 0 || n_prefix < 0 ||
-      cloud_stride < n_prefix)
+  if ((dtype != FFPS_F32 && dtype != FFPS_F64 && dtype != FFPS_F32_F64) || batch < 0 ||
+      n_prefix < 0 || cloud_stride < n_prefix)
     return fail(FFPS_EINVAL, "h2d_prefix: bad arguments");
   if (batch == 0 || n_prefix == 0) return FFPS_OK;
   if (!dst || !src_host) return fail(FFPS_EINVAL, "null pointer");
-  const size_t esz = dtype == FFPS_F32 ? 4 : 8;
+  const size_t esz = dtype == FFPS_F64 ? 8 : 4;  // coordinates as stored
   cudaError_t e = cudaMemcpy2DAsync(dst, (size_t)n_prefix * 3 * esz, src_host,
                                     (size_t)cloud_stride * 3 * esz, (size_t)n_prefix * 3 * esz,
                                     (size_t)batch, cudaMemcpyHostToDevice,
@@ -750,13 +812,76 @@ int ffps_auto_schedule(int64_t n, int64_t batch) {
   return FFPS_ALGO_GRID_CL(grid_cluster(a, batch, device_info(dev).sms, n));
 }
 
-int ffps_run_kernel_ex(int dtype, const void* xyz, int64_t batch, int64_t cloud_stride,
-                       int64_t n, int64_t iters, const int64_t* seed_pos,
-                       const int64_t* index_map, int64_t map_stride, int64_t* order,
-                       void* sel_d2, int64_t out_stride, void* stream, int algo) {
+}  // extern "C"
+
+namespace {
+
+bool valid_dtype(int dtype) {
+  return dtype == FFPS_F32 || dtype == FFPS_F64 || dtype == FFPS_F32_F64;
+}
+
+int dispatch(int dtype, const void* xyz, int64_t batch, int64_t cloud_stride, int64_t n,
+             int64_t iters, const int64_t* seed_pos, const int64_t* index_map,
+             int64_t map_stride, int64_t* order, void* sel_d2, int64_t out_stride,
+             cudaStream_t st, int dev, int a, bool from_auto, int64_t* stats);
+
+// FFPS_F32_F64 on a schedule without float-coordinate kernels: widen the rows
+// the run can read (the prefix [0, n), or the whole cloud for restricted
+// runs) into binary64 scratch, then run the binary64 kernels on it
+int run_widened(const void* xyz, int64_t batch, int64_t cloud_stride, int64_t n, int64_t iters,
+                const int64_t* seed_pos, const int64_t* index_map, int64_t map_stride,
+                int64_t* order, void* sel_d2, int64_t out_stride, cudaStream_t st, int dev,
+                int a) {
+  const int64_t rows = index_map ? cloud_stride : n;
+  void* wide = nullptr;
+  cudaError_t e = ffps::scratch_alloc(&wide, (size_t)batch * rows * 3 * sizeof(double), st);
+  if (e != cudaSuccess) return cuda_fail(e, "scratch_alloc(widen)");
+  e = ffps::launch_upcast(xyz, batch, cloud_stride, rows, wide, device_info(dev).sms, st);
+  if (e != cudaSuccess) {
+    ffps::scratch_free(wide, st);
+    return cuda_fail(e, "upcast_kernel launch");
+  }
+  const int rc = dispatch(FFPS_F64, wide, batch, rows, n, iters, seed_pos, index_map, map_stride,
+                          order, sel_d2, out_stride, st, dev, a, false, nullptr);
+  e = ffps::scratch_free(wide, st);
+  if (rc != FFPS_OK) return rc;
+  if (e != cudaSuccess) return cuda_fail(e, "scratch_free(widen)");
+  g_last_launches += 1;
+  return FFPS_OK;
+}
+
+int dispatch(int dtype, const void* xyz, int64_t batch, int64_t cloud_stride, int64_t n,
+             int64_t iters, const int64_t* seed_pos, const int64_t* index_map,
+             int64_t map_stride, int64_t* order, void* sel_d2, int64_t out_stride,
+             cudaStream_t st, int dev, int a, bool from_auto, int64_t* stats) {
+  if ((a & 0xff) == FFPS_ALGO_GRID) {
+    const int rc = run_grid(dtype, xyz, batch, cloud_stride, n, iters, seed_pos, index_map,
+                            map_stride, order, sel_d2, out_stride, st, dev, a, stats);
+    if (rc != FFPS_EUNSUPPORTED || !from_auto) return rc;
+    // AUTO: the cloud's bucket table does not fit shared memory -> the
+    // streaming kernel, which spills the points beyond the cluster to HBM
+    a = FFPS_ALGO_STREAM;
+  }
+  if (dtype == FFPS_F32_F64)
+    return run_widened(xyz, batch, cloud_stride, n, iters, seed_pos, index_map, map_stride,
+                       order, sel_d2, out_stride, st, dev, a);
+  if (a == FFPS_ALGO_BUCKET || a == FFPS_ALGO_MULTI)
+    return run_bucketed(dtype, xyz, batch, cloud_stride, n, iters, seed_pos, index_map,
+                        map_stride, order, sel_d2, out_stride, st, dev, a == FFPS_ALGO_MULTI);
+  if (a == FFPS_ALGO_SMALL && n <= kSmallMax)  // larger clouds: the streaming kernel
+    return run_small(dtype, xyz, batch, cloud_stride, n, iters, seed_pos, index_map, map_stride,
+                     order, sel_d2, out_stride, st);
+  return run_streaming(dtype, xyz, batch, cloud_stride, n, iters, seed_pos, index_map,
+                       map_stride, order, sel_d2, out_stride, st, dev);
+}
+
+int run_kernel_impl(int dtype, const void* xyz, int64_t batch, int64_t cloud_stride, int64_t n,
+                    int64_t iters, const int64_t* seed_pos, const int64_t* index_map,
+                    int64_t map_stride, int64_t* order, void* sel_d2, int64_t out_stride,
+                    void* stream, int algo, int64_t* stats) {
   g_last_launches = 0;
-  if (dtype != FFPS_F32 && dtype != FFPS_F64)
-    return fail(FFPS_EINVAL, "dtype must be FFPS_F32 or FFPS_F64");
+  if (!valid_dtype(dtype))
+    return fail(FFPS_EINVAL, "dtype must be FFPS_F32, FFPS_F64 or FFPS_F32_F64");
   if (algo != FFPS_ALGO_AUTO && algo != FFPS_ALGO_STREAM && algo != FFPS_ALGO_BUCKET &&
       algo != FFPS_ALGO_MULTI && algo != FFPS_ALGO_GRID && algo != FFPS_ALGO_GRID_CL(1) &&
       algo != FFPS_ALGO_GRID_CL(2) && algo != FFPS_ALGO_GRID_CL(4) && algo != FFPS_ALGO_SMALL)
@@ -774,19 +899,31 @@ int ffps_run_kernel_ex(int dtype, const void* xyz, int64_t batch, int64_t cloud_
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int a = resolve_algo(algo, n, batch);
-  if ((a & 0xff) == FFPS_ALGO_GRID)
-    return run_grid(dtype, xyz, batch, cloud_stride, n, iters, seed_pos, index_map, map_stride,
-                    order, sel_d2, out_stride, st, dev, a);
-  if (a == FFPS_ALGO_BUCKET || a == FFPS_ALGO_MULTI)
-    return run_bucketed(dtype, xyz, batch, cloud_stride, n, iters, seed_pos, index_map,
-                        map_stride, order, sel_d2, out_stride, st, dev, a == FFPS_ALGO_MULTI);
-  if (a == FFPS_ALGO_SMALL && n <= kSmallMax)  // larger clouds: the streaming kernel
-    return run_small(dtype, xyz, batch, cloud_stride, n, iters, seed_pos, index_map, map_stride,
-                     order, sel_d2, out_stride, st);
-  return run_streaming(dtype, xyz, batch, cloud_stride, n, iters, seed_pos, index_map,
-                       map_stride, order, sel_d2, out_stride, st, dev);
+  return dispatch(dtype, xyz, batch, cloud_stride, n, iters, seed_pos, index_map, map_stride,
+                  order, sel_d2, out_stride, static_cast<cudaStream_t>(stream), dev, a,
+                  algo == FFPS_ALGO_AUTO, stats);
+}
+
+}  // namespace
+
+extern "C" {
+
+int ffps_run_kernel_ex(int dtype, const void* xyz, int64_t batch, int64_t cloud_stride,
+                       int64_t n, int64_t iters, const int64_t* seed_pos,
+                       const int64_t* index_map, int64_t map_stride, int64_t* order,
+                       void* sel_d2, int64_t out_stride, void* stream, int algo) {
+  return run_kernel_impl(dtype, xyz, batch, cloud_stride, n, iters, seed_pos, index_map,
+                         map_stride, order, sel_d2, out_stride, stream, algo, nullptr);
+}
+
+int ffps_run_kernel_stats(int dtype, const void* xyz, int64_t batch, int64_t cloud_stride,
+                          int64_t n, int64_t iters, const int64_t* seed_pos,
+                          const int64_t* index_map, int64_t map_stride, int64_t* order,
+                          void* sel_d2, int64_t out_stride, void* stream, int algo,
+                          int64_t* stats) {
+  return run_kernel_impl(dtype, xyz, batch, cloud_stride, n, iters, seed_pos, index_map,
+                         map_stride, order, sel_d2, out_stride, stream, algo, stats);
 }
 
 int ffps_run_kernel(int dtype, const void* xyz, int64_t batch, int64_t cloud_stride, int64_t n,
@@ -801,8 +938,8 @@ int ffps_coverage(int dtype, const void* xyz, int64_t batch, int64_t cloud_strid
                   const int64_t* idx, int64_t idx_stride, int64_t m, void* out_d2,
                   void* stream) {
   g_last_launches = 0;
-  if (dtype != FFPS_F32 && dtype != FFPS_F64)
-    return fail(FFPS_EINVAL, "dtype must be FFPS_F32 or FFPS_F64");
+  if (!valid_dtype(dtype))
+    return fail(FFPS_EINVAL, "dtype must be FFPS_F32, FFPS_F64 or FFPS_F32_F64");
   if (batch < 0 || n < 1 || n > 0x7fffffffLL || m < 1 || m > 0x7fffffffLL)
     return fail(FFPS_EINVAL, "coverage: bad sizes");
   if (batch == 0) return FFPS_OK;
@@ -813,6 +950,20 @@ int ffps_coverage(int dtype, const void* xyz, int64_t batch, int64_t cloud_strid
   if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
   const DeviceInfo di = device_info(dev);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (dtype == FFPS_F32_F64) {  // binary64 on the widened cloud (exact)
+    void* wide = nullptr;
+    e = ffps::scratch_alloc(&wide, (size_t)batch * n * 3 * sizeof(double), st);
+    if (e != cudaSuccess) return cuda_fail(e, "scratch_alloc(widen)");
+    e = ffps::launch_upcast(xyz, batch, cloud_stride, n, wide, di.sms, st);
+    int rc = e == cudaSuccess ? ffps_coverage(FFPS_F64, wide, batch, n, n, idx, idx_stride, m,
+                                              out_d2, stream)
+                              : cuda_fail(e, "upcast_kernel launch");
+    const int64_t l = g_last_launches + 1;
+    e = ffps::scratch_free(wide, st);
+    if (rc == FFPS_OK && e != cudaSuccess) rc = cuda_fail(e, "scratch_free(widen)");
+    g_last_launches = rc == FFPS_OK ? l : 0;
+    return rc;
+  }
   const size_t esz = dtype == FFPS_F32 ? 4 : 8;
   // sample buckets: boxes staged in shared memory -> bucket size from the budget
   int64_t bss = 32;
@@ -824,9 +975,9 @@ int ffps_coverage(int dtype, const void* xyz, int64_t batch, int64_t cloud_strid
   const size_t per_p = (size_t)nsp * (7 * esz + 8) + (size_t)nbp * 6 * esz;
   const size_t per_s = (size_t)nss * (7 * esz + 8) + (size_t)nbs * 6 * esz;
   unsigned char* scratch = nullptr;
-  e = cudaMallocAsync(reinterpret_cast<void**>(&scratch), (per_p + per_s) * (size_t)batch + 1024,
+  e = ffps::scratch_alloc(reinterpret_cast<void**>(&scratch), (per_p + per_s) * (size_t)batch + 1024,
                       st);
-  if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync(coverage)");
+  if (e != cudaSuccess) return cuda_fail(e, "scratch_alloc(coverage)");
   auto carve = [&](unsigned char* base, int64_t nslots, int64_t nb, int64_t bs,
                    ffps::BucketBuildParams& bb) {
     const size_t arr = (size_t)nslots * esz * (size_t)batch;
@@ -888,9 +1039,9 @@ int ffps_coverage(int dtype, const void* xyz, int64_t batch, int64_t cloud_strid
     e = ffps::launch_coverage(dtype, cp, batch, di.sms, st);
     if (e == cudaSuccess) ++launches;
   }
-  cudaError_t e2 = cudaFreeAsync(scratch, st);
+  cudaError_t e2 = ffps::scratch_free(scratch, st);
   if (e != cudaSuccess) return cuda_fail(e, "coverage launch");
-  if (e2 != cudaSuccess) return cuda_fail(e2, "cudaFreeAsync(coverage)");
+  if (e2 != cudaSuccess) return cuda_fail(e2, "scratch_free(coverage)");
   g_last_launches = launches;
   return FFPS_OK;
 }
@@ -898,8 +1049,9 @@ int ffps_coverage(int dtype, const void* xyz, int64_t batch, int64_t cloud_strid
 int ffps_fill_slice(int dtype, int64_t* order, void* sel_d2, int64_t batch, int64_t out_stride,
                     int64_t k, int64_t m1, void* stream) {
   g_last_launches = 0;
-  if (dtype != FFPS_F32 && dtype != FFPS_F64)
-    return fail(FFPS_EINVAL, "dtype must be FFPS_F32 or FFPS_F64");
+  if (!valid_dtype(dtype))
+    return fail(FFPS_EINVAL, "dtype must be FFPS_F32, FFPS_F64 or FFPS_F32_F64");
+  if (dtype == FFPS_F32_F64) dtype = FFPS_F64;  // sel_d2 is binary64
   if (batch < 0 || k < 1 || m1 < k || out_stride < m1)
     return fail(FFPS_EINVAL, "fill: need 1 <= k <= m1 <= out_stride");
   if (batch == 0 || m1 == k) return FFPS_OK;
@@ -915,8 +1067,9 @@ int ffps_fill_random(int dtype, int64_t* order, void* sel_d2, int64_t batch, int
                      int64_t n, int64_t k, int64_t m1, uint64_t state_hi, uint64_t state_lo,
                      uint64_t inc_hi, uint64_t inc_lo, void* stream) {
   g_last_launches = 0;
-  if (dtype != FFPS_F32 && dtype != FFPS_F64)
-    return fail(FFPS_EINVAL, "dtype must be FFPS_F32 or FFPS_F64");
+  if (!valid_dtype(dtype))
+    return fail(FFPS_EINVAL, "dtype must be FFPS_F32, FFPS_F64 or FFPS_F32_F64");
+  if (dtype == FFPS_F32_F64) dtype = FFPS_F64;  // sel_d2 is binary64
   if (batch < 0 || k < 1 || m1 < k || out_stride < m1 || n < m1)
     return fail(FFPS_EINVAL, "fill: need 1 <= k <= m1 <= min(n, out_stride)");
   if (n >= 0x7fffffffLL) return fail(FFPS_EUNSUPPORTED, "fill: n must be < 2^31");
@@ -925,18 +1078,18 @@ int ffps_fill_random(int dtype, int64_t* order, void* sel_d2, int64_t batch, int
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int64_t words = ffps::fill_random_scratch_words(n, k, m1);
   uint32_t* scratch = nullptr;
-  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&scratch),
+  cudaError_t e = ffps::scratch_alloc(reinterpret_cast<void**>(&scratch),
                                   (size_t)words * 4 * (size_t)batch, st);
-  if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync(fill_random)");
+  if (e != cudaSuccess) return cuda_fail(e, "scratch_alloc(fill_random)");
   const uint64_t pcg[4] = {state_hi, state_lo, inc_hi, inc_lo};
   // FFPS_FILL_SEQUENTIAL=1 (tests): the single-thread generator that backs up
   // the warp-parallel one when Lemire rejections outrun its value stream
   const char* seq = getenv("FFPS_FILL_SEQUENTIAL");
   e = ffps::launch_fill_random(dtype, order, sel_d2, batch, out_stride, n, k, m1, pcg, scratch,
                                st, seq && strcmp(seq, "1") == 0);
-  cudaError_t e2 = cudaFreeAsync(scratch, st);
+  cudaError_t e2 = ffps::scratch_free(scratch, st);
   if (e != cudaSuccess) return cuda_fail(e, "fill_random_kernel launch");
-  if (e2 != cudaSuccess) return cuda_fail(e2, "cudaFreeAsync(fill_random)");
+  if (e2 != cudaSuccess) return cuda_fail(e2, "scratch_free(fill_random)");
   g_last_launches = 1;
   return FFPS_OK;
 }

@@ -80,7 +80,11 @@ __global__ void __launch_bounds__(kBuildThreads, 1) bucket_build_kernel(const Bu
   T* X = static_cast<T*>(p.X) + base;
   T* Y = static_cast<T*>(p.Y) + base;
   T* Z = static_cast<T*>(p.Z) + base;
-  T* D = static_cast<T*>(p.D) + base;
+  // D is T, or double under FFPS_F32_F64 (float coordinates, binary64 keys)
+  auto put_d = [&](int64_t i, T v) {
+    if (sizeof(T) == 4 && p.d_wide) static_cast<double*>(p.D)[base + i] = (double)v;
+    else static_cast<T*>(p.D)[base + i] = v;
+  };
   int32_t* O = p.O + base;
   T* BB = static_cast<T*>(p.BB) + (int64_t)b * p.nbuckets * 6;
 
@@ -197,7 +201,7 @@ __global__ void __launch_bounds__(kBuildThreads, 1) bucket_build_kernel(const Bu
     X[s] = x;
     Y[s] = y;
     Z[s] = z;
-    D[s] = pinf;
+    put_d(s, pinf);
     O[s] = i;
   }
   __syncthreads();  // global writes of the block visible to the block
@@ -297,7 +301,7 @@ __global__ void __launch_bounds__(kBuildThreads, 1) bucket_build_kernel(const Bu
     X[s] = X[first_last];
     Y[s] = Y[first_last];
     Z[s] = Z[first_last];
-    D[s] = -pinf;
+    put_d(s, -pinf);
     O[s] = -1;
   }
   __syncthreads();

@@ -564,7 +564,11 @@ __global__ void __launch_bounds__(256) bucket_kd_leaves_kernel(const BucketBuild
                    static_cast<T*>(p.Z) + base, p.O + base};
   const Bufs<T> tmp{static_cast<T*>(p.TX) + base, static_cast<T*>(p.TY) + base,
                     static_cast<T*>(p.TZ) + base, p.TO + base};
-  T* D = static_cast<T*>(p.D) + base;
+  // D is T, or double under FFPS_F32_F64 (float coordinates, binary64 keys)
+  auto put_d = [&](int64_t i, T v) {
+    if (sizeof(T) == 4 && p.d_wide) static_cast<double*>(p.D)[base + i] = (double)v;
+    else static_cast<T*>(p.D)[base + i] = v;
+  };
   T* BB = static_cast<T*>(p.BB) + (int64_t)b * p.nbuckets * 6;
   const T pinf = (T)INFINITY;
 
@@ -657,7 +661,7 @@ __global__ void __launch_bounds__(256) bucket_kd_leaves_kernel(const BucketBuild
           out.z[st + i] = v2;
           out.o[st + i] = src.o[st + i];
         }
-        D[st + i] = pinf;
+        put_d(st + i, pinf);
         if (i == 0) {
           f0 = v0;
           f1 = v1;
@@ -676,7 +680,7 @@ __global__ void __launch_bounds__(256) bucket_kd_leaves_kernel(const BucketBuild
           out.x[s] = f0;
           out.y[s] = f1;
           out.z[s] = f2;
-          D[s] = -pinf;
+          put_d(s, -pinf);
           out.o[s] = -1;
         }
       }
@@ -841,7 +845,7 @@ cudaError_t launch_bucket_kd(int dtype, const BucketBuildParams& p, int64_t batc
   const size_t hdr_b = (size_t)batch * 2 * 4, sm_b = (size_t)batch * kMaxSeg * 2 * 4;
   const size_t box_b = (size_t)batch * kMaxSeg * 6 * esz;
   unsigned char* segs = nullptr;
-  e = cudaMallocAsync(reinterpret_cast<void**>(&segs), hdr_b + sm_b + box_b + 64, st);
+  e = scratch_alloc(reinterpret_cast<void**>(&segs), hdr_b + sm_b + box_b + 64, st);
   if (e != cudaSuccess) return e;
   int32_t* seg_hdr = reinterpret_cast<int32_t*>(segs);
   int32_t* seg_sm = reinterpret_cast<int32_t*>(segs + hdr_b);
@@ -884,7 +888,7 @@ cudaError_t launch_bucket_kd(int dtype, const BucketBuildParams& p, int64_t batc
     e = cudaLaunchKernel(f2, dim3((unsigned)((kMaxSeg + wpc - 1) / wpc), (unsigned)batch),
                          dim3(32 * wpc), a2, leaves_smem, st);
   }
-  cudaError_t e2 = cudaFreeAsync(segs, st);
+  cudaError_t e2 = scratch_free(segs, st);
   return e != cudaSuccess ? e : e2;
 }
 

@@ -77,6 +77,7 @@ struct BucketBuildParams {
   int64_t bs;           // points per bucket
   void *TX, *TY, *TZ;   // [batch][nslots] scratch for the second sort level (or null)
   int32_t* TO;
+  int d_wide;           // 1: D is double while the coordinates are float (FFPS_F32_F64)
 };
 
 struct BucketParams {
@@ -98,6 +99,7 @@ struct BucketParams {
   float neg_zero;  // -0.0f, opaque to ptxas (sq2)
   long long* trace;     // optional phase trace (FFPS_TRACE_BUCKET), else null
   int64_t trace_iters;
+  long long* stats;     // optional [batch][4] counters (K1g, ffps_run_kernel_stats), else null
 };
 
 struct BucketInst {
@@ -114,15 +116,18 @@ const BucketInst* multi_instances(int* count);  // K1m (fps_multi.cu)
 
 // K1g (fps_grid.cu): multi-winner rounds with a cell index of the buckets
 struct GridInst {
-  int dtype;
+  int dtype;       // 0 f32, 1 f64, 2 f32 coordinates + binary64 arithmetic
   int nt;
   int ppl;
   int km;          // winners per round at most
   int cl;          // CTAs per cloud (thread-block cluster size)
   const void* fn;  // fps_grid_kernel(BucketParams)
-  size_t esz;
+  size_t esz;      // bytes per stored coordinate
 };
-const GridInst* grid_instances(int* count);
+const GridInst* grid_instances(int* count);  // all of the three below
+const GridInst* grid_instances_f32(int* count);
+const GridInst* grid_instances_f64(int* count);
+const GridInst* grid_instances_mixed(int* count);
 size_t grid_smem(int dtype, int64_t nb);
 size_t bucket_build_smem();
 size_t bucket_kd_smem();
@@ -143,6 +148,17 @@ struct CoverageParams {
 };
 cudaError_t launch_coverage(int dtype, const CoverageParams& p, int64_t batch, int sms,
                             cudaStream_t st);
+
+// FFPS_F32_F64 on kernels without a float-coordinate variant: widen the
+// [batch][cloud_stride][3] float rows [0, rows) into dense [batch][rows][3]
+// doubles (convert.cu).
+cudaError_t launch_upcast(const void* src, int64_t batch, int64_t cloud_stride, int64_t rows,
+                          void* dst, int sms, cudaStream_t st);
+
+// Library scratch: stream-ordered allocations from a private per-device pool
+// (abi.cu), so the device's default pool and its attributes stay the caller's.
+cudaError_t scratch_alloc(void** p, size_t bytes, cudaStream_t st);
+cudaError_t scratch_free(void* p, cudaStream_t st);
 
 // K2: slice fill (fill.cu).
 cudaError_t launch_fill_slice(int dtype, int64_t* order, void* sel_d2, int64_t batch,

@@ -74,6 +74,11 @@ def run_kernel(points: NDArray[np.float64], m: int, seed_pos: int, threads: int 
     if pts.dtype not in (np.float32, np.float64):
         pts = pts.astype(np.float64)
     n = int(pts.shape[0])
+    if not 0 <= int(seed_pos) < n:
+        # the reference indexes dist[seed_pos] (fps_core.py:130): IndexError
+        # past the end; a negative position is rejected here as well, before
+        # any kernel reads xyz[seed]
+        raise IndexError(f"seed position {seed_pos} is out of bounds for {n} points")
     dev = _device.require_cuda()
     xyz = torch.from_numpy(np.array(pts, order="C")).to(dev).unsqueeze(0)
     order = torch.empty((1, m), dtype=torch.int64, device=dev)

@@ -31,10 +31,11 @@ def _as_index_array(sample) -> np.ndarray:
     return np.asarray(sample, dtype=np.int64)
 
 
-def coverage_d2_batch(xyz, indices, *, device=None) -> torch.Tensor:
+def coverage_d2_batch(xyz, indices, *, device=None, precision=None) -> torch.Tensor:
     """Squared covering radius of every cloud: ``xyz`` (B, N, 3), ``indices``
-    (B, M) int64 sample indices.  Returns (B,) in the input dtype, on the
-    device (max over points of min over samples of d2)."""
+    (B, M) int64 sample indices.  Returns (B,) on the device (max over points
+    of min over samples of d2), in the input dtype — or binary64 with
+    ``precision="f64"`` on float32 clouds (the reference's arithmetic)."""
     x = as_device_batch(xyz, device)
     idx = indices if isinstance(indices, torch.Tensor) else \
         torch.from_numpy(np.ascontiguousarray(np.asarray(indices, dtype=np.int64)))
@@ -50,14 +51,16 @@ def coverage_d2_batch(xyz, indices, *, device=None) -> torch.Tensor:
     bad = (idx < 0) | (idx >= x.shape[1])
     if bool(bad.any()):
         raise IndexError(f"sample index out of range for a cloud of {x.shape[1]} points")
-    out = torch.empty(x.shape[0], dtype=x.dtype, device=x.device)
+    from .batched import _out_dtype
+    out = torch.empty(x.shape[0], dtype=_out_dtype(x, precision), device=x.device)
     _device.coverage(x, idx, out)
     return out
 
 
-def coverage_radius_batch(xyz, indices, *, device=None) -> torch.Tensor:
+def coverage_radius_batch(xyz, indices, *, device=None, precision=None) -> torch.Tensor:
     """(B,) float64 covering radii, sqrt taken in binary64 (metrics.py:52)."""
-    return torch.sqrt(coverage_d2_batch(xyz, indices, device=device).to(torch.float64))
+    return torch.sqrt(coverage_d2_batch(xyz, indices, device=device,
+                                        precision=precision).to(torch.float64))
 
 
 def coverage_radius(sample, cloud: PointCloud) -> float:

@@ -29,5 +29,29 @@ def test_clouds_are_deterministic():
 
 
 def test_cpu_sample_runs():
-    dt, cnt = bench.cpu_pipeline_sample(24_000, bench.BUDGETS[24_000], 0.75, 2, "uniform", 2)
-    assert cnt == 2 and dt > 0
+    for dtype in ("f64", "f32"):
+        dt, cnt = bench.cpu_pipeline_sample(24_000, bench.BUDGETS[24_000], 0.75, 2, "uniform", 2,
+                                            dtype)
+        assert cnt == 2 and dt > 0
+
+
+def test_shards_cover_the_global_batch():
+    """Strong scaling splits the BASELINE global batch of 64 by cloud; --batch
+    gives B clouds per rank (weak)."""
+    for world in (1, 2, 4, 8):
+        got = [bench.shard(bench.parse([]), world, r) for r in range(world)]
+        assert sum(c for _, c, _, _ in got) == 64
+        assert [f for f, _, _, _ in got] == [64 // world * r for r in range(world)]
+        assert all(gb == 64 and sc == "strong" for _, _, gb, sc in got)
+    f, c, gb, sc = bench.shard(bench.parse(["--batch", "16"]), 4, 3)
+    assert (f, c, gb, sc) == (48, 16, 64, "weak")
+
+
+def test_gpus_flag_must_match_world(monkeypatch):
+    """--gpus is authoritative: a torchrun world of another size fails loudly."""
+    import pytest
+    monkeypatch.setenv("WORLD_SIZE", "2")
+    monkeypatch.setattr("sys.argv", ["bench.py", "--gpus", "4"])
+    with pytest.raises(SystemExit) as ei:
+        bench.main()
+    assert "WORLD_SIZE=2" in str(ei.value)
