@@ -19,6 +19,7 @@ from .fps_core import OrderedSample, SamplerStats, fps, run_kernel
 from .fps_prune import FillMode, PruneConfig, candidate_prune, fps_prune
 from .geometry import Point3, PointCloud, squared_distance, validate_cloud
 from .metrics import coverage_d2_batch, coverage_radius, coverage_radius_batch
+from .pnn import flashfps_hierarchy, furthest_point_sample
 
 __version__ = "0.1.0"
 
@@ -27,7 +28,8 @@ __all__ = [
     "OrderedSample", "Point3", "PointCloud", "PrefixCheckResult", "PruneConfig",
     "SamplerStats", "cache_footprint", "candidate_prune", "coverage_d2_batch",
     "coverage_radius", "coverage_radius_batch", "errors", "fps", "fps_batch",
-    "fps_prune", "fps_prune_batch", "hierarchical_sample", "hierarchical_sample_batch",
+    "flashfps_hierarchy", "fps_prune", "fps_prune_batch", "furthest_point_sample",
+    "hierarchical_sample", "hierarchical_sample_batch",
     "hierarchical_sample_detailed", "hierarchical_sample_host", "prefix_reuse", "read_cache",
     "run_kernel", "run_restricted", "run_restricted_batch", "squared_distance",
     "validate_cloud", "verify_prefix_property", "write_cache", "write_cache_text",

@@ -23,6 +23,8 @@ def main():
                     choices=["multi", "grid", "grid@1", "grid@2", "grid@4"])
     ap.add_argument("--cloud", choices=["uniform", "lidar"], default="uniform")
     ap.add_argument("--cloud-n", type=int, default=200000)
+    ap.add_argument("--precision", choices=["f32", "f64"], default="f32",
+                    help="f64: binary64 arithmetic on the float coordinates (FFPS_F32_F64)")
     a = ap.parse_args()
     if a.cloud == "lidar":  # the bench's LiDAR frames, candidate prefix of n points
         import bench
@@ -37,7 +39,8 @@ def main():
     prev = _device.set_schedule(a.sched)
     B = a.batch
     order = torch.empty((B, a.iters), dtype=torch.int64, device="cuda")
-    sel = torch.empty((B, a.iters), dtype=x.dtype, device="cuda")
+    sel = torch.empty((B, a.iters), dtype=torch.float64 if a.precision == "f64" else x.dtype,
+                      device="cuda")
     seeds = torch.zeros(B, dtype=torch.int64, device="cuda")
     _device.greedy(x, a.n, a.iters, seeds, order, sel)
     torch.cuda.synchronize()
