@@ -110,6 +110,19 @@ __device__ __forceinline__ double box_lb(double px, double py, double pz, const 
   return __dadd_rn(__dadd_rn(__dmul_rn(gx, gx), __dmul_rn(gy, gy)), __dmul_rn(gz, gz));
 }
 
+// Lower bound of the binary64 box_lb above, in binary32 with every operation
+// rounded down, for float coordinates p and a float box (FFPS_F32_F64).
+// Per step RD32(x) <= the exact value and RN64 of anything at least as large
+// is >= it (RD32(x) is a double <= x), so box_lb_rd <= box_lb(double).
+// Testing box_lb_rd >= RU32(key) therefore skips only buckets the binary64
+// test skips (it may flag a few more; re-evaluating them changes nothing).
+__device__ __forceinline__ float box_lb_rd(float px, float py, float pz, const float* b) {
+  const float gx = fmaxf(fmaxf(__fsub_rd(b[0], px), __fsub_rd(px, b[3])), 0.0f);
+  const float gy = fmaxf(fmaxf(__fsub_rd(b[1], py), __fsub_rd(py, b[4])), 0.0f);
+  const float gz = fmaxf(fmaxf(__fsub_rd(b[2], pz), __fsub_rd(pz, b[5])), 0.0f);
+  return __fadd_rd(__fadd_rd(__fmul_rd(gx, gx), __fmul_rd(gy, gy)), __fmul_rd(gz, gz));
+}
+
 }  // namespace
 
 // dynamic shared memory bytes of fps_grid_kernel for nb buckets (per CTA);
@@ -120,6 +133,7 @@ __host__ __device__ constexpr size_t grid_smem_bytes(int64_t nb) {
                        4 /*ki*/ + 4 /*pmask*/ + 4 /*rlist*/) +
          (size_t)((nb + kGS - 1) / kGS) *
              (6 * sizeof(S) + 6 * sizeof(typename Arith<T>::bits_t) + 14 * 4) +  // NCG <= 4
+         (size_t)(nb + (nb + kGS - 1) / kGS) * 4 +  // binary32 shadow keys (FFPS_F32_F64)
          16;  // alignment of the coordinate arrays after the keys
 }
 
@@ -234,6 +248,11 @@ __global__ void __launch_bounds__(NT, 1) fps_grid_kernel(const BucketParams prm)
   uint32_t* cand_p = reinterpret_cast<uint32_t*>(rlist + nb);  // [NCG ng]
   int32_t* cand_q = reinterpret_cast<int32_t*>(cand_p + NCG * ng);  // [NCG ng]
   int32_t* gdirty = cand_q + NCG * ng;  // [ng] group has a re-evaluated bucket this round
+  // FFPS_F32_F64: the flag phase tests in binary32, rounded down, against the
+  // keys rounded up (box_lb_rd): shadow keys of the buckets and group maxima
+  constexpr bool SHADOW = sizeof(T) == 8 && sizeof(S) == 4;
+  float* kv32 = reinterpret_cast<float*>(gdirty + ng + ng);  // [nb] (after dlist)
+  float* gmax32 = kv32 + nb;                                 // [ng]
   int32_t* dlist = gdirty + ng;       // [ng] dirty groups
   // phase D: per-warp candidate list (<= 32)
   __shared__ bits_t cv_w[1][64];
@@ -254,11 +273,19 @@ __global__ void __launch_bounds__(NT, 1) fps_grid_kernel(const BucketParams prm)
   // accepted points of the last round: every warp keeps its own copy (all
   // warps derive the same set from the candidate list, no barrier needed)
   __shared__ T sp_w[1][KM][3];
+  __shared__ float sp32_w[SHADOW ? KM : 1][3];  // the same points as float (exact, SHADOW)
   __shared__ uint32_t si_w[1][KM];
   __shared__ int32_t sq_w[1][KM];
   __shared__ int16_t top_w[1][KM];
   __shared__ int acc_s;
   __shared__ bits_t rmax_s;
+  // chain test: the ranked candidates' coordinates and bucket bounds,
+  // broadcast from shared memory (cheaper than 4-8 shuffles per pair)
+  struct __align__(16) ChainRec {
+    T x, y, z;
+    bits_t b2;
+  };
+  __shared__ ChainRec ch_s[KM];
   __shared__ int rcount_s, npair_s, ndirty_s;
   __shared__ int pair_s[KM * 128];  // flag phase: (point << 16 | group) pairs
   __shared__ T ext_s;
@@ -279,6 +306,7 @@ __global__ void __launch_bounds__(NT, 1) fps_grid_kernel(const BucketParams prm)
       hi[c] = bh > hi[c] ? bh : hi[c];
     }
     kv[q] = k2[q] = A::bits(A::pinf());
+    if constexpr (SHADOW) kv32[q] = __int_as_float(0x7f800000);
     ki[q] = kNoIdx;
     kx[q * 3 + 0] = kx[q * 3 + 1] = kx[q * 3 + 2] = S(0);
     pmask[q] = 0u;
@@ -333,6 +361,7 @@ __global__ void __launch_bounds__(NT, 1) fps_grid_kernel(const BucketParams prm)
       gbox[g * 6 + 3 + c] = z[c];
     }
     gmax[g] = A::bits(A::pinf());
+    if constexpr (SHADOW) gmax32[g] = __int_as_float(0x7f800000);
     gdirty[g] = 0;
   }
   __syncthreads();
@@ -348,6 +377,8 @@ __global__ void __launch_bounds__(NT, 1) fps_grid_kernel(const BucketParams prm)
     sp_w[0][0][0] = (T)X0[3 * src + 0];
     sp_w[0][0][1] = (T)X0[3 * src + 1];
     sp_w[0][0][2] = (T)X0[3 * src + 2];
+    if constexpr (SHADOW)
+      for (int c = 0; c < 3; ++c) sp32_w[0][c] = (float)X0[3 * src + c];
     si_w[0][0] = (uint32_t)seed;
     sq_w[0][0] = -1;
   }
@@ -375,18 +406,26 @@ __global__ void __launch_bounds__(NT, 1) fps_grid_kernel(const BucketParams prm)
     const uint32_t old = atomicOr(&pmask[q], 1u << t);
     if (old == 0u) rlist[atomicAdd(&rcount_s, 1)] = q;
   };
-  auto test = [&](int q, int t, T px, T py, T pz) {  // K1b's exact bound test
-    if (!(box_lb(px, py, pz, box + (size_t)q * 6) >= A::from_bits(kv[q]))) flag(q, t);
+  // does point t reach bucket q's key?  (K1b's exact bound test; SHADOW: its
+  // binary32 lower bound against the key rounded up, a superset of hits)
+  auto reaches = [&](int q, int t) -> bool {
+    if constexpr (SHADOW)
+      return !(box_lb_rd(sp32_w[t][0], sp32_w[t][1], sp32_w[t][2], box + (size_t)q * 6) >=
+               kv32[q]);
+    else
+      return !(box_lb(sp_w[0][t][0], sp_w[0][t][1], sp_w[0][t][2], box + (size_t)q * 6) >=
+               A::from_bits(kv[q]));
+  };
+  auto test = [&](int q, int t) {
+    if (reaches(q, t)) flag(q, t);
   };
   // warp-converged variant for two (point, bucket) tests per lane (two pairs of
   // the flag phase in flight): every lane calls it; new buckets are appended
   // with one shared-memory atomic per warp.  (An L2 -> L1 prefetch of the new
   // buckets' points here was measured 3% slower and dropped.)
   auto test_warp2 = [&](bool v0, int q0, int t0, bool v1, int q1, int t1) {
-    const bool h0 = v0 && !(box_lb(sp_w[0][t0][0], sp_w[0][t0][1], sp_w[0][t0][2],
-                                   box + (size_t)q0 * 6) >= A::from_bits(kv[q0]));
-    const bool h1 = v1 && !(box_lb(sp_w[0][t1][0], sp_w[0][t1][1], sp_w[0][t1][2],
-                                   box + (size_t)q1 * 6) >= A::from_bits(kv[q1]));
+    const bool h0 = v0 && reaches(q0, t0);
+    const bool h1 = v1 && reaches(q1, t1);
     const bool n0 = h0 && atomicOr(&pmask[q0], 1u << t0) == 0u;
     const bool n1 = h1 && atomicOr(&pmask[q1], 1u << t1) == 0u;
     const unsigned m0 = __ballot_sync(0xffffffffu, n0), m1 = __ballot_sync(0xffffffffu, n1);
@@ -456,7 +495,7 @@ __global__ void __launch_bounds__(NT, 1) fps_grid_kernel(const BucketParams prm)
           flag(q, 0);
           continue;
         }
-        for (int t = 0; t < J; ++t) test(q, t, sp_w[0][t][0], sp_w[0][t][1], sp_w[0][t][2]);
+        for (int t = 0; t < J; ++t) test(q, t);
       }
       if (round > 0 && warp == 0 && lane < J && sq_w[0][lane] >= 0 &&
           sq_w[0][lane] % CL == rank)
@@ -470,10 +509,15 @@ __global__ void __launch_bounds__(NT, 1) fps_grid_kernel(const BucketParams prm)
 #pragma unroll 1
       for (int tw = warp; tw < (J <= kWppJ ? J * wpp : J); tw += NW) {
         const int t = J <= kWppJ ? c_wpp.t[J][tw] : tw, sub = J <= kWppJ ? c_wpp.s[J][tw] : 0;
-        const T px = sp_w[0][t][0], py = sp_w[0][t][1], pz = sp_w[0][t][2];
         for (int g0 = sub * 32; g0 < ng; g0 += wpp * 32) {
           const int g = g0 + lane;
-          const bool hit = g < ng && !(box_lb(px, py, pz, gbox + (size_t)g * 6) >= A::from_bits(gmax[g]));
+          bool hit;
+          if constexpr (SHADOW)
+            hit = g < ng && !(box_lb_rd(sp32_w[t][0], sp32_w[t][1], sp32_w[t][2],
+                                        gbox + (size_t)g * 6) >= gmax32[g]);
+          else
+            hit = g < ng && !(box_lb(sp_w[0][t][0], sp_w[0][t][1], sp_w[0][t][2],
+                                     gbox + (size_t)g * 6) >= A::from_bits(gmax[g]));
           const unsigned m = __ballot_sync(0xffffffffu, hit);
           ntest_w += __popc(m);
           if (m) {
@@ -571,6 +615,7 @@ __global__ void __launch_bounds__(NT, 1) fps_grid_kernel(const BucketParams prm)
         const bits_t w2 = A::warp_max(lane == wl ? b2 : b1);
         if (lane == wl) {
           kv[q] = b1;
+          if constexpr (SHADOW) kv32[q] = __double2float_ru(A::from_bits(b1));
           ki[q] = i1;
           k2[q] = w2;
           kx[q * 3 + 0] = x1;
@@ -629,7 +674,10 @@ __global__ void __launch_bounds__(NT, 1) fps_grid_kernel(const BucketParams prm)
           taken |= wk;
           if (wk & (1u << lane)) v = A::kmin;
           if (lane == 0) {
-            if (k == 0) gmax[g] = mk;
+            if (k == 0) {
+              gmax[g] = mk;
+              if constexpr (SHADOW) gmax32[g] = __double2float_ru(A::from_bits(mk));
+            }
             cand_v[NCG * g + k] = mk;
             cand_p[NCG * g + k] = pk;
             cand_q[NCG * g + k] = wk ? g * kGS + __ffs(wk) - 1 : 0;
@@ -929,15 +977,27 @@ __global__ void __launch_bounds__(NT, 1) fps_grid_kernel(const BucketParams prm)
       // key to any earlier accepted candidate and beats their buckets' second best
       const bool live = lane < nc;
       bool ok = live && A::from_bits(cv) >= T(0);
+#ifdef FFPS_GRID_CHAIN_SHFL
 #pragma unroll
       for (int bb = 0; bb < KM - 1; ++bb) {
         const T bx = __shfl_sync(0xffffffffu, cx, bb);
         const T by = __shfl_sync(0xffffffffu, cy, bb);
         const T bz = __shfl_sync(0xffffffffu, cz, bb);
         const bits_t b2 = A::shfl(c2, bb);
-        const bool cond = !(A::d2(cx, cy, cz, bx, by, bz) < A::from_bits(cv)) && cv > b2;  // (a), (b)
-        ok = ok && (bb >= lane || cond);
+        const bool ca = !(A::d2(cx, cy, cz, bx, by, bz) < A::from_bits(cv));
+        ok = ok & ((bb >= lane) | (ca & (cv > b2)));
       }
+#else
+      if (lane < KM) ch_s[lane] = ChainRec{cx, cy, cz, c2};
+      __syncwarp();
+#pragma unroll
+      for (int bb = 0; bb < KM - 1; ++bb) {
+        const ChainRec cb = ch_s[bb];
+        // (a), (b); evaluated for every lane without branches (bitwise ops)
+        const bool ca = !(A::d2(cx, cy, cz, cb.x, cb.y, cb.z) < A::from_bits(cv));
+        ok = ok & ((bb >= lane) | (ca & (cv > cb.b2)));
+      }
+#endif
       const unsigned okm = __ballot_sync(0xffffffffu, ok || lane == 0);
       acc = __ffs(~okm) - 1;
       if (acc < 0 || acc > nc) acc = nc;
@@ -947,6 +1007,11 @@ __global__ void __launch_bounds__(NT, 1) fps_grid_kernel(const BucketParams prm)
         sp_w[0][lane][0] = cx;
         sp_w[0][lane][1] = cy;
         sp_w[0][lane][2] = cz;
+        if constexpr (SHADOW) {
+          sp32_w[lane][0] = (float)cx;  // float coordinates: exact
+          sp32_w[lane][1] = (float)cy;
+          sp32_w[lane][2] = (float)cz;
+        }
         si_w[0][lane] = cpos;
         sq_w[0][lane] = cq;
         if (rank == 0) {
