@@ -115,7 +115,8 @@ enum ffps_algo { FFPS_ALGO_AUTO = 0, FFPS_ALGO_STREAM = 1, FFPS_ALGO_BUCKET = 2,
  * when `stats` (device, [batch][FFPS_STATS_WORDS] int64, caller-zeroed) is not
  * NULL the GRID schedule writes, per cloud, the rounds of its greedy loop,
  * the SM cycles the loop took on cluster rank 0, the buckets re-evaluated and
- * the points loaded by those re-evaluations (summed over the cluster's CTAs);
+ * the rounds whose candidate ranking took the general path (both summed over
+ * the cluster's CTAs);
  * other schedules leave it untouched.  Used to report the latency roofline
  * (cycles per round) next to the kernel time. */
 #define FFPS_STATS_WORDS 4

@@ -60,8 +60,9 @@ class grid_stats:
     """Context manager that attaches a per-cloud counter block to every greedy
     launch issued inside it (ffps_run_kernel_stats); ``records`` holds
     (batch, n, iters, stats) with stats a (batch, 4) int64 device tensor:
-    rounds, loop cycles on cluster rank 0, re-evaluated buckets, points
-    loaded by the re-evaluations (grid schedule only; zeros otherwise)."""
+    rounds, loop cycles on cluster rank 0, re-evaluated buckets, rounds
+    ranked through the general path, summed over the cluster's CTAs (grid
+    schedule only; zeros otherwise)."""
 
     def __enter__(self):
         global _stats

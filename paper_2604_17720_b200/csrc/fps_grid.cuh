@@ -475,6 +475,7 @@ __global__ void __launch_bounds__(NT, 1) fps_grid_kernel(const BucketParams prm)
   // counters (prm.stats): rounds, loop cycles on rank 0, re-evaluated buckets
   const long long loop_t0 = clock64();
   long long nflag = 0;
+  int ngeneral = 0;  // rounds whose ranking took the general path (warp 0)
   int round = 0;
   for (; k < iters; ++round) {
     long long t0 = 0, t1 = 0, t2 = 0, t3 = 0;
@@ -871,6 +872,7 @@ __global__ void __launch_bounds__(NT, 1) fps_grid_kernel(const BucketParams prm)
         }
       }
       ncand_w = nct | (general ? 1 << 16 : 0);
+      ngeneral += general ? 1 : 0;
       if (trace) td[3] = clock64();
     }
     __syncwarp();
@@ -1048,7 +1050,7 @@ __global__ void __launch_bounds__(NT, 1) fps_grid_kernel(const BucketParams prm)
       st[1] = (unsigned long long)(clock64() - loop_t0);
     }
     atomicAdd(st + 2, (unsigned long long)nflag);
-    atomicAdd(st + 3, (unsigned long long)(nflag * BS));
+    atomicAdd(st + 3, (unsigned long long)ngeneral);
   }
   if constexpr (CL > 1) cluster_sync_all();  // no rank leaves while peers may push into it
   // positions -> original indices for restricted runs (fps_cache.py:197)
