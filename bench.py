@@ -600,19 +600,25 @@ def latency_roofline(args, x, budgets, cfg_flash, prec, kern, clocks, B) -> dict
     rounds = float(st[:, 0].mean())
     cycles = float(st[:, 1].mean())
     flagged = float(st[:, 2].mean())
-    # floor: minimal table, same instance family (KM, CL, bucket size 32)
-    nf = 1024 * (int(sched.split("@")[1]) if "@" in sched else 1)
+    general = float(st[:, 3].mean()) / max(1, int(sched.split("@")[1]) if "@" in sched else 1)
+    # floor: the same kernel instance (KM = 16, CL, 32-point buckets) on the
+    # smallest table that keeps the standard ranking path: KM bucket groups
+    # of 32 buckets per CTA (fewer groups than KM make every round take the
+    # general path), a quarter of the points as iterations (the C5 ratio)
+    cl = int(sched.split("@")[1]) if "@" in sched else 1
+    nf = 32 * 32 * 16 * cl
     floor_x = x[:, :nf].contiguous()
     prev = _device.set_schedule(sched)
     try:
         with _device.grid_stats() as gf:
-            ffps.fps_batch(floor_x, nf // 2, precision=prec)
+            ffps.fps_batch(floor_x, nf // 4, precision=prec)
             torch.cuda.synchronize()
     finally:
         _device.set_schedule(prev)
     sf = gf.records[0][3].double()
     f_rounds = float(sf[:, 0].mean())
     f_cycles = float(sf[:, 1].mean())
+    f_general = float(sf[:, 3].mean()) / cl
     floor_cpr = f_cycles / max(f_rounds, 1.0)
     cpr = cycles / max(rounds, 1.0)
     kms = float(np.mean([k[3] for k in kern if k[1] == c1])) if kern else float("nan")
@@ -627,8 +633,10 @@ def latency_roofline(args, x, budgets, cfg_flash, prec, kern, clocks, B) -> dict
             "rounds_per_cloud": rounds, "winners_per_round": (k1 - 1) / max(rounds, 1.0),
             "cycles_per_round": cpr, "floor_cycles_per_round": floor_cpr,
             "frac_cycles": floor_cpr / cpr,
-            "floor": f"same kernel, {nf}-point clouds (one bucket group per CTA), "
-                     f"{nf // 2} iterations, {B} clouds: {f_rounds:.0f} rounds",
+            "floor": f"same kernel, {nf}-point clouds (16 bucket groups per CTA), "
+                     f"{nf // 4} iterations, {B} clouds: {f_rounds:.0f} rounds, "
+                     f"{f_general:.0f} through the general ranking path",
+            "general_path_rounds_per_cloud": general,
             "buckets_reevaluated_per_round": flagged / max(rounds, 1.0),
             "sm_mhz": sm_mhz,
             "streaming_equivalent": {

@@ -10,8 +10,8 @@ selection distances against the C oracle (pinned to the reference's goldens):
 * binary64 (double coordinates) at the full C2 and C3 FlashFPS shapes;
 * LiDAR-like frames (bench.lidar_cloud) at the C3 and C5 stage-1 shapes on
   K1g with 1 and 2 CTAs per cloud, where the candidate ranking takes its
-  general path in a large share of rounds (asserted from the kernel
-  counters)."""
+  general path in tens to hundreds of rounds per cloud (asserted from the
+  kernel counters)."""
 
 import numpy as np
 import pytest
@@ -132,6 +132,6 @@ def test_lidar_flash_stage1_general_path(cuda, lidar_frames, shape, sched, preci
     wo, ws = oracle.run_kernel_batch(x.astype(np.float64) if precision else x, k, seeds, n=c)
     _assert_same(go, gs, wo, ws, f"LiDAR {shape} {sched} {precision or 'f32'}")
     rounds, general = st[:, 0], st[:, 3]
-    cl = int(sched[-1])
-    # the general ranking path ran in a sizeable share of rounds (per CTA)
-    assert (general / cl >= 0.1 * rounds).all(), (rounds, general)
+    # the general ranking path ran (C5 LiDAR: ~6% of the rounds per CTA on one
+    # CTA per cloud, ~11% on two; C3: more)
+    assert (general >= 20).all() and (general < rounds * int(sched[-1])).all(), (rounds, general)
