@@ -628,7 +628,7 @@ def latency_roofline(args, x, budgets, cfg_flash, prec, kern, clocks, B) -> dict
     units = B * c1 * (k1 - 1)
     return {"bound": "latency", "achieved": achieved, "peak": peak,
             "unit": "greedy rounds/s per cloud", "frac": achieved / peak,
-            "traffic": dram_traffic("fps_grid_kernel"),
+            "traffic": dram_traffic("fps_grid_kernel", prec),
             "kernel": "fps_grid_kernel (K1g) " + sched, "kernel_ms": kms,
             "rounds_per_cloud": rounds, "winners_per_round": (k1 - 1) / max(rounds, 1.0),
             "cycles_per_round": cpr, "floor_cycles_per_round": floor_cpr,
@@ -646,13 +646,15 @@ def latency_roofline(args, x, budgets, cfg_flash, prec, kern, clocks, B) -> dict
                 "gbs": units * BYTES_PER_UNIT[prec] / (kms / 1e3) / 1e9}}
 
 
-def dram_traffic(kname: str):
+def dram_traffic(kname: str, prec: str = "f64"):
     """Per-launch DRAM bytes of a kernel from one `ncu --set full` capture
-    (profiles/traffic.json), or None."""
+    (profiles/traffic.json), or None: the instance of the headline's
+    arithmetic (float coordinates + binary64 = <double, float, ...>) first."""
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
             tj = json.load(fh)
-        hit = [v for k_, v in tj.items() if kname in k_ and "F32_F64" in k_] or \
+        tag = "<double, float," if prec == "f64" else "<float,"
+        hit = [v for k_, v in tj.items() if kname in k_ and tag in k_] or \
               [v for k_, v in tj.items() if kname in k_]
         return hit[0]["dram_bytes"] if hit else None
     except (OSError, ValueError, KeyError):

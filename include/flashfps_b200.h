@@ -168,6 +168,29 @@ int ffps_fill_random(int dtype, int64_t* order, void* sel_d2, int64_t batch,
                      uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi,
                      uint64_t inc_lo, void* stream);
 
+/* The whole FlashFPS pyramid in one call (replaces hierarchical_sample /
+ * hierarchical_sample_detailed, fps_cache.py:204-256, with FPS-Prune layer 1,
+ * fps_prune.py:68-111): layer 1 = greedy over the candidate prefix xyz[b][0:c)
+ * for k iterations (k, c = PruneConfig.kernel_budget / candidate_count,
+ * computed by the caller in IEEE double, fps_prune.py:45-51) followed by the
+ * budget fill of [k, budgets[0]) (fill_mode 0 = DETERMINISTIC_SLICE, 1 =
+ * SEEDED_RANDOM with pcg = NumPy's PCG64(rng_seed) state {state_hi, state_lo,
+ * inc_hi, inc_lo}); with cache_enabled the deeper layers are prefixes of
+ * layer 1 (fps_cache.py:141-148: order[l], sel_d2[l] for l >= 1 are not
+ * written and may be NULL); without it layer l re-runs exact FPS over layer
+ * l-1's points in their order, seeded at position 0 (fps_cache.py:189-201),
+ * reported in original indices.
+ *   budgets   HOST [nlayers], non-increasing, >= 1
+ *   seed_pos  DEVICE [batch] layer-1 seed positions (< c)
+ *   order     HOST array of nlayers DEVICE pointers, order[l] = [batch][budgets[l]] int64
+ *   sel_d2    HOST array of nlayers DEVICE pointers, [batch][budgets[l]] (dtype's result type)
+ * Stream-ordered launches, no host synchronisation. */
+int ffps_hierarchical_sample(int dtype, const void* xyz, int64_t batch, int64_t cloud_stride,
+                             int64_t n, const int64_t* budgets, int nlayers, int64_t k,
+                             int64_t c, int fill_mode, const uint64_t* pcg,
+                             int cache_enabled, const int64_t* seed_pos, int64_t* const* order,
+                             void* const* sel_d2, void* stream);
+
 /* Covering radius of samples (replaces coverage_radius / _min_dist2_to,
  * metrics.py:29-52): out_d2[b] = max over p in xyz[b][0:n) of min over
  * i < m of d2(p, xyz[b][idx[b][i]]), the reference's rounded d2; the caller

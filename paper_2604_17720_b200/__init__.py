@@ -10,7 +10,7 @@ benchmark and by point-network callers.
 
 from . import errors
 from .batched import (BatchSample, fps_batch, fps_prune_batch, hierarchical_sample_batch,
-                      hierarchical_sample_host, run_restricted_batch)
+                      hierarchical_sample_fused, hierarchical_sample_host, run_restricted_batch)
 from .fps_cache import (BYTES_PER_ENTRY, CacheRecord, LayerBudgets, PrefixCheckResult,
                         cache_footprint, hierarchical_sample, hierarchical_sample_detailed,
                         prefix_reuse, read_cache, run_restricted, verify_prefix_property,
@@ -30,7 +30,7 @@ __all__ = [
     "coverage_radius", "coverage_radius_batch", "errors", "fps", "fps_batch",
     "flashfps_hierarchy", "fps_prune", "fps_prune_batch", "furthest_point_sample",
     "hierarchical_sample", "hierarchical_sample_batch",
-    "hierarchical_sample_detailed", "hierarchical_sample_host", "prefix_reuse", "read_cache",
+    "hierarchical_sample_detailed", "hierarchical_sample_fused", "hierarchical_sample_host", "prefix_reuse", "read_cache",
     "run_kernel", "run_restricted", "run_restricted_batch", "squared_distance",
     "validate_cloud", "verify_prefix_property", "write_cache", "write_cache_text",
     "__version__",

@@ -44,6 +44,9 @@ SIGNATURES = {
     "ffps_run_kernel_stats": (_int, [_int, _vp, _i64, _i64, _i64, _i64, _vp, _vp, _i64, _vp,
                                      _vp, _i64, _vp, _int, _vp]),
     "ffps_trim_scratch": (_int, []),
+    "ffps_hierarchical_sample": (_int, [_int, _vp, _i64, _i64, _i64, ctypes.POINTER(_i64), _int,
+                                        _i64, _i64, _int, ctypes.POINTER(ctypes.c_uint64), _int,
+                                        _vp, ctypes.POINTER(_vp), ctypes.POINTER(_vp), _vp]),
     "ffps_fill_slice": (_int, [_int, _vp, _vp, _i64, _i64, _i64, _i64, _vp]),
     "ffps_fill_random": (_int, [_int, _vp, _vp, _i64, _i64, _i64, _i64, _i64, ctypes.c_uint64,
                                 ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64, _vp]),
@@ -100,6 +103,27 @@ def run_kernel(dtype, xyz, batch, cloud_stride, n, iters, seed_pos, index_map, m
                                        index_map, map_stride, order, sel_d2, out_stride, stream,
                                        ALGO[algo], stats)
     check(rc, "ffps_run_kernel")
+    return int(lib.ffps_last_launch_count())
+
+
+def hierarchical_sample(dtype, xyz, batch, cloud_stride, n, budgets, k, c, fill_mode, pcg_state,
+                        cache_enabled, seed_pos, orders, sels, stream) -> int:
+    """ffps_hierarchical_sample: ``orders``/``sels`` are per-layer device
+    pointers (None where not written); ``pcg_state`` = (state, inc) or None."""
+    lib = load()
+    L = len(budgets)
+    b = (_i64 * L)(*budgets)
+    if pcg_state is not None:
+        m64 = (1 << 64) - 1
+        st, inc = pcg_state
+        pcg = (ctypes.c_uint64 * 4)((st >> 64) & m64, st & m64, (inc >> 64) & m64, inc & m64)
+    else:
+        pcg = None
+    o = (_vp * L)(*orders)
+    s = (_vp * L)(*sels)
+    check(lib.ffps_hierarchical_sample(dtype, xyz, batch, cloud_stride, n, b, L, k, c, fill_mode,
+                                       pcg, int(bool(cache_enabled)), seed_pos, o, s, stream),
+          "ffps_hierarchical_sample")
     return int(lib.ffps_last_launch_count())
 
 

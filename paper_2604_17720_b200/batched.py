@@ -39,8 +39,8 @@ from .fps_core import OrderedSample, SamplerStats
 from .fps_prune import FillMode, PruneConfig
 
 __all__ = ["BatchSample", "as_device_batch", "fps_batch", "fps_prune_batch",
-           "run_restricted_batch", "hierarchical_sample_batch", "hierarchical_sample_host",
-           "cache_footprint_bytes"]
+           "run_restricted_batch", "hierarchical_sample_batch", "hierarchical_sample_fused",
+           "hierarchical_sample_host", "cache_footprint_bytes"]
 
 BYTES_PER_ENTRY = 36  # fps_cache.py:28 (uint32 index + 3 x f64 + f64 dist2)
 
@@ -275,6 +275,61 @@ def hierarchical_sample_batch(xyz, budgets: Sequence[int], cfg: PruneConfig, see
             s, st = _run_restricted_device(x, layers[-1].indices, m, zero, precision)
             layers.append(s)
             per_layer.append(st)
+    total = SamplerStats(
+        distance_evals=sum(s.distance_evals for s in per_layer),
+        iterations=sum(s.iterations for s in per_layer),
+        candidates=sum(s.candidates for s in per_layer),
+        cache_bytes=sum(s.cache_bytes for s in per_layer))
+    return layers, total, per_layer
+
+
+def hierarchical_sample_fused(xyz, budgets: Sequence[int], cfg: PruneConfig, seed_index=0,
+                              cache_enabled: bool = True, *, device=None, precision=None):
+    """hierarchical_sample_batch through ONE C-ABI call
+    (ffps_hierarchical_sample): the greedy layer 1, its fill and, with the
+    cache off, every restricted deeper layer are issued by the library on
+    the current stream without returning to Python.  Same results and return
+    value as hierarchical_sample_batch."""
+    from . import _native
+    b = _budgets(budgets)
+    B, n = _shape(xyz)
+    if b[0] > n:
+        raise BudgetExceedsCloud(f"M1={b[0]} exceeds cloud size {n}")
+    seeds = _seed_array(seed_index, B)
+    k, c = _fps_prune_checks(B, n, b[0], cfg, seeds)
+    x = as_device_batch(xyz, device)
+    od = _out_dtype(x, precision)
+    orders = [torch.empty((B, m), dtype=torch.int64, device=x.device)
+              for m in (b if not cache_enabled else b[:1])]
+    sels = [torch.empty((B, m), dtype=od, device=x.device)
+            for m in (b if not cache_enabled else b[:1])]
+    pcg = None
+    if cfg.fill_mode is not FillMode.DETERMINISTIC_SLICE and b[0] > k:
+        st = np.random.PCG64(cfg.rng_seed).state["state"]
+        pcg = (int(st["state"]), int(st["inc"]))
+    sel_code = torch.empty(0, dtype=od)
+    with torch.cuda.device(x.device):
+        _device._count(_native.hierarchical_sample(
+            _device.dtype_code(x, sel_code), x.data_ptr(), B, x.shape[1], n, list(b), k, c,
+            0 if pcg is None else 1, pcg, cache_enabled,
+            _device.seeds_tensor(seeds, B, x.device).data_ptr(),
+            [t.data_ptr() for t in orders] + [None] * (len(b) - len(orders)),
+            [t.data_ptr() for t in sels] + [None] * (len(b) - len(sels)),
+            torch.cuda.current_stream(x.device).cuda_stream))
+    layer1 = BatchSample(orders[0], sels[0], k)
+    stats1 = SamplerStats(distance_evals=c * (k - 1), iterations=k, candidates=c)
+    layers, per_layer = [layer1], [stats1]
+    if cache_enabled:
+        stats1.cache_bytes = cache_footprint_bytes(b[0])
+        for m in b[1:]:
+            layers.append(BatchSample(layer1.indices[:, :m], layer1.selection_dist2[:, :m],
+                                      min(k, m)))
+            per_layer.append(SamplerStats())
+    else:
+        for li, m in enumerate(b[1:], 1):
+            layers.append(BatchSample(orders[li], sels[li], m))
+            per_layer.append(SamplerStats(distance_evals=b[li - 1] * (m - 1), iterations=m,
+                                          candidates=b[li - 1]))
     total = SamplerStats(
         distance_evals=sum(s.distance_evals for s in per_layer),
         iterations=sum(s.iterations for s in per_layer),

@@ -1094,4 +1094,59 @@ int ffps_fill_random(int dtype, int64_t* order, void* sel_d2, int64_t batch, int
   return FFPS_OK;
 }
 
+int ffps_hierarchical_sample(int dtype, const void* xyz, int64_t batch, int64_t cloud_stride,
+                             int64_t n, const int64_t* budgets, int nlayers, int64_t k,
+                             int64_t c, int fill_mode, const uint64_t* pcg,
+                             int cache_enabled, const int64_t* seed_pos, int64_t* const* order,
+                             void* const* sel_d2, void* stream) {
+  if (!budgets || nlayers < 1 || !order || !sel_d2)
+    return fail(FFPS_EINVAL, "hierarchical_sample: need budgets and per-layer outputs");
+  const int64_t m1 = budgets[0];
+  for (int l = 0; l < nlayers; ++l) {
+    if (budgets[l] < 1 || (l > 0 && budgets[l] > budgets[l - 1]))  // fps_cache.py:42-50
+      return fail(FFPS_EINVAL, "budgets must be >= 1 and non-increasing");
+    if ((l == 0 || !cache_enabled) && (!order[l] || !sel_d2[l]))
+      return fail(FFPS_EINVAL, "layer %d output is NULL", l);
+  }
+  if (m1 > n || k < 1 || k > m1 || c < k || c > n)  // fps_prune.py:45-51,78-88
+    return fail(FFPS_EINVAL, "need 1 <= k <= m1 <= n and k <= c <= n");
+  if (fill_mode != 0 && fill_mode != 1) return fail(FFPS_EINVAL, "fill_mode must be 0 or 1");
+  if (fill_mode == 1 && m1 > k && !pcg) return fail(FFPS_EINVAL, "random fill needs the PCG64 state");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  int64_t launches = 0;
+  // layer 1: FPS-Prune = greedy over the candidate prefix, then the fill
+  int rc = run_kernel_impl(dtype, xyz, batch, cloud_stride, c, k, seed_pos, nullptr, 0, order[0],
+                           sel_d2[0], m1, stream, FFPS_ALGO_AUTO, nullptr);
+  if (rc != FFPS_OK) return rc;
+  launches += g_last_launches;
+  if (m1 > k) {
+    rc = fill_mode == 0 ? ffps_fill_slice(dtype, order[0], sel_d2[0], batch, m1, k, m1, stream)
+                        : ffps_fill_random(dtype, order[0], sel_d2[0], batch, m1, n, k, m1,
+                                           pcg[0], pcg[1], pcg[2], pcg[3], stream);
+    if (rc != FFPS_OK) return rc;
+    launches += g_last_launches;
+  }
+  // cache off: every deeper layer re-runs exact FPS over the previous layer's
+  // points in its order, seeded at position 0 (fps_cache.py:227-232,189-201);
+  // K0 gathers them through the previous layer's indices
+  if (!cache_enabled && nlayers > 1) {
+    int64_t* zeros = nullptr;
+    cudaError_t e = ffps::scratch_alloc(reinterpret_cast<void**>(&zeros),
+                                        (size_t)batch * sizeof(int64_t), st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(zeros, 0, (size_t)batch * sizeof(int64_t), st);
+    if (e != cudaSuccess) return cuda_fail(e, "hierarchical_sample: seed scratch");
+    for (int l = 1; l < nlayers && rc == FFPS_OK; ++l) {
+      rc = run_kernel_impl(dtype, xyz, batch, cloud_stride, budgets[l - 1], budgets[l], zeros,
+                           order[l - 1], budgets[l - 1], order[l], sel_d2[l], budgets[l], stream,
+                           FFPS_ALGO_AUTO, nullptr);
+      launches += g_last_launches;
+    }
+    e = ffps::scratch_free(zeros, st);
+    if (rc != FFPS_OK) return rc;
+    if (e != cudaSuccess) return cuda_fail(e, "scratch_free(seeds)");
+  }
+  g_last_launches = launches;
+  return FFPS_OK;
+}
+
 }  // extern "C"

@@ -582,6 +582,7 @@ __global__ void __launch_bounds__(256) bucket_kd_leaves_kernel(const BucketBuild
 
   const int st0 = seg_sm[((int64_t)b * kMaxSeg + s0) * 2 + 0];
   const int m0 = seg_sm[((int64_t)b * kMaxSeg + s0) * 2 + 1];
+  FFPS_CHECK(cap == 0 || m0 <= cap);  // the staged segment fits its buffers
   Bufs<T> P0, P1;
   if (cap > 0) {
     // stage the segment with four TMA bulk copies (x, y, z, o; 16-B aligned:

@@ -404,7 +404,11 @@ __global__ void __launch_bounds__(NT, 1) fps_grid_kernel(const BucketParams prm)
 
   auto flag = [&](int q, int t) {  // OR point t into bucket q's mask, list it once
     const uint32_t old = atomicOr(&pmask[q], 1u << t);
-    if (old == 0u) rlist[atomicAdd(&rcount_s, 1)] = q;
+    if (old == 0u) {
+      const int e = atomicAdd(&rcount_s, 1);
+      FFPS_CHECK(e < nb);
+      rlist[e] = q;
+    }
   };
   // does point t reach bucket q's key?  (K1b's exact bound test; SHADOW: its
   // binary32 lower bound against the key rounded up, a superset of hits)
@@ -435,6 +439,7 @@ __global__ void __launch_bounds__(NT, 1) fps_grid_kernel(const BucketParams prm)
       if (lane == 0) base = atomicAdd(&rcount_s, c0 + __popc(m1));
       base = __shfl_sync(0xffffffffu, base, 0);
       const unsigned below = (1u << lane) - 1u;
+      FFPS_CHECK(base + c0 + __popc(m1) <= nb);
       if (n0) rlist[base + __popc(m0 & below)] = q0;
       if (n1) rlist[base + c0 + __popc(m1 & below)] = q1;
     }
@@ -525,6 +530,7 @@ __global__ void __launch_bounds__(NT, 1) fps_grid_kernel(const BucketParams prm)
             int base = 0;
             if (lane == __ffs(m) - 1) base = atomicAdd(&npair_s, __popc(m));
             base = __shfl_sync(0xffffffffu, base, __ffs(m) - 1);
+            FFPS_CHECK(base + __popc(m) <= KM * 128);
             if (hit) pair_s[base + __popc(m & ((1u << lane) - 1u))] = (t << 16) | g;
           }
         }
@@ -561,6 +567,7 @@ __global__ void __launch_bounds__(NT, 1) fps_grid_kernel(const BucketParams prm)
       uint32_t os[CH][PPL];
 #pragma unroll
       for (int c = 0; c < CH; ++c) {
+        FFPS_CHECK(e0 + c * NW < nr);
         qc[c] = rlist[e0 + c * NW];
         pm[c] = pmask[qc[c]];
 #pragma unroll
@@ -713,6 +720,7 @@ __global__ void __launch_bounds__(NT, 1) fps_grid_kernel(const BucketParams prm)
         for (int o = 1; o < 16; o <<= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
         if (part == 0 && v != A::kmin) {
           if (cnt < KM) {
+            FFPS_CHECK(g < ng && cnt >= 0);
             topg_s[cnt] = g;
             grank_s[g] = (int16_t)cnt;
 #pragma unroll
@@ -749,6 +757,7 @@ __global__ void __launch_bounds__(NT, 1) fps_grid_kernel(const BucketParams prm)
         for (int o = 1; o < TPC; o <<= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
         if (part == 0) rr_s[c] = v != A::kmin ? cnt : 0x7fffffff;
         if (part == 0 && v != A::kmin && cnt < KM) {
+          FFPS_CHECK(compq_s[c] >= 0 && compq_s[c] < nb);
           top_s[cnt] = (int16_t)compq_s[c];
           topv_s[cnt] = v;
         }

@@ -4,6 +4,17 @@
 #pragma once
 #include <cstdint>
 
+// Debug builds (tools/build_variant.sh checks -DFFPS_DEBUG_CHECKS): device
+// asserts on the shared-memory list bounds of the kernels.  compute-sanitizer
+// is closed on this GPU pool, so these asserts plus the parity suites are the
+// race / bounds evidence.
+#ifdef FFPS_DEBUG_CHECKS
+#include <cassert>
+#define FFPS_CHECK(c) assert(c)
+#else
+#define FFPS_CHECK(c) ((void)0)
+#endif
+
 namespace ffps {
 
 __device__ __forceinline__ uint32_t cluster_ctarank() {

@@ -156,3 +156,24 @@ def test_precision_argument_checks(cuda):
         ffps.fps_batch(x, 3, precision="f32")
     with pytest.raises(ValueError):
         ffps.fps_batch(x.float(), 3, precision="f16")
+
+
+@pytest.mark.parametrize("precision", [None, "f64"])
+@pytest.mark.parametrize("cache", [True, False])
+@pytest.mark.parametrize("fill", ["slice", "random"])
+def test_fused_hierarchy_abi_equals_python_pipeline(cuda, precision, cache, fill):
+    """ffps_hierarchical_sample (one C call for the whole pyramid) returns
+    exactly hierarchical_sample_batch's layers and counters."""
+    rng = np.random.default_rng(17)
+    xd = torch.from_numpy(_cloud(rng, 5, 24000, "ties", np.float32)).cuda()
+    cfg = ffps.PruneConfig(p=0.75, rng_seed=9, fill_mode=ffps.FillMode.DETERMINISTIC_SLICE
+                           if fill == "slice" else ffps.FillMode.SEEDED_RANDOM)
+    budgets = (6000, 1500, 375, 93)
+    seeds = np.array([0, 5, 17, 3, 100])
+    a, ta, pa = ffps.hierarchical_sample_batch(xd, budgets, cfg, seeds, cache, precision=precision)
+    b, tb, pb = ffps.hierarchical_sample_fused(xd, budgets, cfg, seeds, cache, precision=precision)
+    for la, lb in zip(a, b):
+        assert torch.equal(la.indices, lb.indices)
+        assert torch.equal(la.selection_dist2, lb.selection_dist2)
+        assert la.fill_boundary == lb.fill_boundary
+    assert vars(ta) == vars(tb) and [vars(x) for x in pa] == [vars(x) for x in pb]
