@@ -88,9 +88,8 @@ int ffps_run_kernel(int dtype, const void* xyz, int64_t batch,
  *                     per cloud; each iteration re-evaluates only the buckets
  *                     whose exact lower bound (same rounded ops) is below
  *                     their max distance;
- *   FFPS_ALGO_MULTI   K0 + K1m: the bucketed schedule taking up to 8 consecutive
- *                     greedy winners per reduction round (the longest prefix of
- *                     the top candidates provably unaffected by each other);
+ *   FFPS_ALGO_MULTI   retired (round 2): the register-table multi-winner K1m was
+ *                     never faster than K1g; the value selects FFPS_ALGO_GRID;
  *   FFPS_ALGO_GRID    K0 + K1g: up to 16 winners per round, the buckets held in
  *                     shared memory and indexed by groups of 32 (kd order), so
  *                     a selected point only tests the buckets within its reach;
@@ -105,7 +104,7 @@ int ffps_run_kernel(int dtype, const void* xyz, int64_t batch,
  *                     batch fits the SMs twice; BUCKET for smaller clouds when
  *                     the batch fills the GPU; SMALL for n <= 8192; else
  *                     STREAM (the environment variable
- *                     FFPS_ALGO=stream|small|bucket|multi|grid overrides
+ *                     FFPS_ALGO=stream|small|bucket|grid overrides
  *                     AUTO). */
 enum ffps_algo { FFPS_ALGO_AUTO = 0, FFPS_ALGO_STREAM = 1, FFPS_ALGO_BUCKET = 2,
                  FFPS_ALGO_MULTI = 3, FFPS_ALGO_GRID = 4, FFPS_ALGO_SMALL = 5 };

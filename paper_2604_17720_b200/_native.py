@@ -26,7 +26,7 @@ if os.environ.get("FFPS_LIB_VARIANT"):
 F32, F64 = 0, 1
 F32_F64 = 2   # float coordinates, binary64 arithmetic (FFPS_F32_F64)
 STATS_WORDS = 4
-ALGO = {"auto": 0, "stream": 1, "bucket": 2, "multi": 3, "grid": 4,
+ALGO = {"auto": 0, "stream": 1, "bucket": 2, "grid": 4,
         # K1g with a fixed number of CTAs per cloud (FFPS_ALGO_GRID_CL(c))
         "grid@1": 4 | 1 << 8, "grid@2": 4 | 2 << 8, "grid@4": 4 | 4 << 8, "small": 5}
 _STATUS = {-1: "EINVAL", -2: "EUNSUPPORTED", -3: "ECUDA"}

@@ -312,11 +312,11 @@ struct BucketPlan {
 
 // Smallest bucket size whose bucket count fits the owned-bucket registers
 // (nt * nbt) and whose per-bucket keys fit shared memory.
-bool make_bucket_plan(int dev, int dtype, int64_t n, BucketPlan* out, bool multi = false) {
+bool make_bucket_plan(int dev, int dtype, int64_t n, BucketPlan* out) {
   const DeviceInfo di = device_info(dev);
   int cnt = 0;
   const ffps::BucketInst* insts =
-      multi ? ffps::multi_instances(&cnt) : ffps::bucket_instances(&cnt);
+      ffps::bucket_instances(&cnt);
   const size_t static_smem = 1024;
   const char* want_nt = getenv("FFPS_BUCKET_NT");  // sweeps: restrict the CTA size
   const int force_nt = want_nt ? atoi(want_nt) : 0;
@@ -353,9 +353,9 @@ size_t box_bytes(int64_t nb, size_t esz, int64_t batch) {
 int run_bucketed(int dtype, const void* xyz, int64_t batch, int64_t cloud_stride, int64_t n,
                  int64_t iters, const int64_t* seed_pos, const int64_t* index_map,
                  int64_t map_stride, int64_t* order, void* sel_d2, int64_t out_stride,
-                 cudaStream_t st, int dev, bool multi) {
+                 cudaStream_t st, int dev) {
   BucketPlan bp;
-  if (!make_bucket_plan(dev, dtype, n, &bp, multi))
+  if (!make_bucket_plan(dev, dtype, n, &bp))
     return fail(FFPS_EUNSUPPORTED, "no bucketed configuration for n=%lld", (long long)n);
   const ffps::BucketInst& k = *bp.inst;
   const int64_t bs = 32 * k.ppl;
@@ -386,11 +386,7 @@ int run_bucketed(int dtype, const void* xyz, int64_t batch, int64_t cloud_stride
   bb.nslots = nslots;
   bb.nbuckets = bp.nbuckets;
   bb.bs = bs;
-  const char* sort2 = getenv("FFPS_BUCKET_SORT2");  // "0": single-level binning (sweeps)
-  if (sort2 && strcmp(sort2, "0") == 0) {
-    bb.TX = bb.TY = bb.TZ = nullptr;
-    bb.TO = nullptr;
-  } else {
+  {
     unsigned char* t = reinterpret_cast<unsigned char*>(bb.O) + (size_t)nslots * 4 * (size_t)batch;
     bb.TX = t;
     bb.TY = t + arr;
@@ -425,7 +421,7 @@ int run_bucketed(int dtype, const void* xyz, int64_t batch, int64_t cloud_stride
   prm.trace_iters = 0;
   prm.stats = nullptr;
   // FFPS_TRACE_BUCKET=<device pointer>,<iterations>: phase trace of CTA 0
-  if (const char* tr = getenv(multi ? "FFPS_TRACE_MULTI" : "FFPS_TRACE_BUCKET")) {
+  if (const char* tr = getenv("FFPS_TRACE_BUCKET")) {
     unsigned long long ptr = 0;
     long long it = 0;
     if (sscanf(tr, "%llu,%lld", &ptr, &it) == 2) {
@@ -740,7 +736,7 @@ int resolve_algo(int algo, int64_t n, int64_t batch) {
     const char* env = getenv("FFPS_ALGO");
     if (env && strcmp(env, "stream") == 0) return FFPS_ALGO_STREAM;
     if (env && strcmp(env, "bucket") == 0) return FFPS_ALGO_BUCKET;
-    if (env && strcmp(env, "multi") == 0) return FFPS_ALGO_MULTI;
+    if (env && strcmp(env, "multi") == 0) return FFPS_ALGO_GRID;  // retired K1m: K1g
     if (env && strcmp(env, "grid") == 0) return FFPS_ALGO_GRID;
     if (env && strcmp(env, "small") == 0) return FFPS_ALGO_SMALL;
     return auto_algo(n, batch);
@@ -865,9 +861,9 @@ int dispatch(int dtype, const void* xyz, int64_t batch, int64_t cloud_stride, in
   if (dtype == FFPS_F32_F64)
     return run_widened(xyz, batch, cloud_stride, n, iters, seed_pos, index_map, map_stride,
                        order, sel_d2, out_stride, st, dev, a);
-  if (a == FFPS_ALGO_BUCKET || a == FFPS_ALGO_MULTI)
+  if (a == FFPS_ALGO_BUCKET)
     return run_bucketed(dtype, xyz, batch, cloud_stride, n, iters, seed_pos, index_map,
-                        map_stride, order, sel_d2, out_stride, st, dev, a == FFPS_ALGO_MULTI);
+                        map_stride, order, sel_d2, out_stride, st, dev);
   if (a == FFPS_ALGO_SMALL && n <= kSmallMax)  // larger clouds: the streaming kernel
     return run_small(dtype, xyz, batch, cloud_stride, n, iters, seed_pos, index_map, map_stride,
                      order, sel_d2, out_stride, st);
@@ -899,7 +895,8 @@ int run_kernel_impl(int dtype, const void* xyz, int64_t batch, int64_t cloud_str
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
-  const int a = resolve_algo(algo, n, batch);
+  // FFPS_ALGO_MULTI (K1m, retired in round 2) runs the multi-winner K1g
+  const int a = resolve_algo(algo == FFPS_ALGO_MULTI ? FFPS_ALGO_GRID : algo, n, batch);
   return dispatch(dtype, xyz, batch, cloud_stride, n, iters, seed_pos, index_map, map_stride,
                   order, sel_d2, out_stride, static_cast<cudaStream_t>(stream), dev, a,
                   algo == FFPS_ALGO_AUTO, stats);

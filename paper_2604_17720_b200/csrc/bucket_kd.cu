@@ -893,4 +893,14 @@ cudaError_t launch_bucket_kd(int dtype, const BucketBuildParams& p, int64_t batc
   return e != cudaSuccess ? e : e2;
 }
 
+// K0 entry points of the bucketed schedules (K1b, K1g, K5): the kd build,
+// two launches (CTA phase + leaf phase).  (The Morton-grid build of round 1
+// was retired in round 2: kd leaves flag 2-4x fewer buckets per point.)
+int bucket_build_launches(const BucketBuildParams&) { return 2; }
+
+cudaError_t launch_bucket_build(int dtype, const BucketBuildParams& p, int64_t batch,
+                                cudaStream_t st) {
+  return launch_bucket_kd(dtype, p, batch, st);
+}
+
 }  // namespace ffps

@@ -60,7 +60,7 @@ inline size_t spill_bytes_per_cta(int dtype, int nt, int g) {
   return static_cast<size_t>(g) * nt * (dtype == 0 ? 16 : 32);
 }
 
-// ---- bucketed path (K0 bucket_build.cu + K1b fps_bucket.cu) ----
+// ---- bucketed path (K0 bucket_kd.cu + K1b fps_bucket.cu, K1g fps_grid*.cu) ----
 constexpr int kBucketThreads = 512;
 
 struct BucketBuildParams {
@@ -112,7 +112,6 @@ struct BucketInst {
 };
 
 const BucketInst* bucket_instances(int* count);
-const BucketInst* multi_instances(int* count);  // K1m (fps_multi.cu)
 
 // K1g (fps_grid.cu): multi-winner rounds with a cell index of the buckets
 struct GridInst {
@@ -129,7 +128,6 @@ const GridInst* grid_instances_f32(int* count);
 const GridInst* grid_instances_f64(int* count);
 const GridInst* grid_instances_mixed(int* count);
 size_t grid_smem(int dtype, int64_t nb);
-size_t bucket_build_smem();
 size_t bucket_kd_smem();
 // kernel launches one launch_bucket_build issues (kd: CTA phase + leaf kernel)
 int bucket_build_launches(const BucketBuildParams& p);

@@ -59,7 +59,7 @@ def test_mixed_random_batches_vs_binary64_oracle(cuda, kind, schedule):
         if kind == "grid":
             N = min(N, 1728)
             m = min(m, N)
-        if schedule in ("stream", "small", "multi") and N > 20000:
+        if schedule in ("stream", "small") and N > 20000:
             continue  # slow schedules: covered up to 20K points
         seeds = rng.integers(0, N, size=B)
         _check_mixed(_cloud(rng, B, N, kind, np.float32), m, seeds)

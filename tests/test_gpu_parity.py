@@ -40,13 +40,13 @@ class _Sched:
             os.environ["FFPS_GRID_KM"] = self.prev_km
 
 
-SCHEDULES = ["stream", "small", "bucket", "multi", "grid", "grid@1", "grid@2", "grid@2/km8"]
+SCHEDULES = ["stream", "small", "bucket", "grid", "grid@1", "grid@2", "grid@2/km8"]
 
 
 @pytest.fixture(params=SCHEDULES)
 def schedule(request):
     """Run the test under each greedy schedule (K1 streaming, K1s small-cloud
-    (n <= 8192, else streaming), K0+K1b bucketed, K1m multi-winner, K1g with 1/2
+    (n <= 8192, else streaming), K0+K1b bucketed, K1g multi-winner with 1/2
     CTAs per cloud)."""
     with _Sched(request.param):
         yield request.param
@@ -288,11 +288,11 @@ def test_abi_rejects_bad_arguments(cuda):
     assert lib.ffps_fill_slice(0, 1, 1, 1, 10, 5, 4, None) == -1
 
 
-@pytest.mark.parametrize("sched", ["bucket", "multi", "grid@1", "grid@2", "grid@4", "grid@1/km8",
+@pytest.mark.parametrize("sched", ["bucket", "grid@1", "grid@2", "grid@4", "grid@1/km8",
                                    "grid@2/km8"])
 @pytest.mark.parametrize("dtype", [np.float32, np.float64])
 def test_bucketed_schedule_sizes_and_ties(cuda, dtype, sched):
-    """K0+K1b / K0+K1m / K1g forced on every size class: n below / at / above
+    """K0+K1b / K1g forced on every size class: n below / at / above
     one bucket, bucket sizes 32/64/128 (n up to 140K), heavy exact ties."""
     with _Sched(sched):
         rng = np.random.default_rng(21)
@@ -306,9 +306,9 @@ def test_bucketed_schedule_sizes_and_ties(cuda, dtype, sched):
 
 
 @pytest.mark.parametrize("dtype", [np.float32, np.float64])
-@pytest.mark.parametrize("sched", ["multi", "grid@1", "grid@2", "grid@4", "grid@2/km8"])
+@pytest.mark.parametrize("sched", ["grid@1", "grid@2", "grid@4", "grid@2/km8"])
 def test_multi_winner_degenerate_ties(cuda, dtype, sched):
-    """K1m when hundreds of bucket keys tie (identical points, exhausted
+    """K1g when hundreds of bucket keys tie (identical points, exhausted
     buckets): the candidate list overflows and rounds fall back to one exact
     winner; results must still match the oracle."""
     with _Sched(sched):

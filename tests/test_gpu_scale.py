@@ -22,7 +22,7 @@ from oracle import oracle
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(params=["stream", "bucket", "multi", "grid"])
+@pytest.fixture(params=["stream", "bucket", "grid"])
 def schedule(request):
     prev = _device.set_schedule(request.param)
     yield request.param

@@ -1,7 +1,7 @@
 #!/usr/bin/env python
 """One small invocation of every kernel family, for compute-sanitizer
 (tools/gpu_sanitize.sh): K1 (stream, cluster/DSMEM/mbarrier), K1s, K0 + K1b,
-K0 + K1m, K0 + K1g with 1/2/4 CTAs per cloud (st.async + mbarrier exchange)
+K0 + K1g with 1/2/4 CTAs per cloud (st.async + mbarrier exchange)
 in binary32, binary64 and binary64-on-float, K2/K2r fills and K5."""
 import os
 import sys
@@ -18,7 +18,7 @@ rng = np.random.default_rng(0)
 x32 = torch.from_numpy(rng.random((2, 3000, 3)).astype(np.float32)).cuda()
 x64 = x32.double()
 runs = []
-for sched in ("stream", "small", "bucket", "multi", "grid@1", "grid@2", "grid@4"):
+for sched in ("stream", "small", "bucket", "grid@1", "grid@2", "grid@4"):
     for name, x, prec in (("f32", x32, None), ("f64", x64, None), ("f32_f64", x32, "f64")):
         runs.append((f"{sched}/{name}", sched, x, prec))
 for tag, sched, x, prec in runs:

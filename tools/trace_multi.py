@@ -1,5 +1,5 @@
 #!/usr/bin/env python
-"""Phase trace of K1m (multi-winner rounds), CTA 0: per round and warp
+"""Phase trace of K1g (multi-winner rounds), CTA 0: per round and warp
 {start, bound test, re-evaluation, warp top-K, after merge}, winners taken
 per round and flagged buckets of the warp."""
 import argparse
@@ -19,8 +19,8 @@ def main():
     ap.add_argument("--n", type=int, default=50000)
     ap.add_argument("--iters", type=int, default=12500)
     ap.add_argument("--nw", type=int, default=16)
-    ap.add_argument("--sched", default="multi",
-                    choices=["multi", "grid", "grid@1", "grid@2", "grid@4"])
+    ap.add_argument("--sched", default="grid@2",
+                    choices=["grid", "grid@1", "grid@2", "grid@4"])
     ap.add_argument("--cloud", choices=["uniform", "lidar"], default="uniform")
     ap.add_argument("--cloud-n", type=int, default=200000)
     ap.add_argument("--precision", choices=["f32", "f64"], default="f32",
