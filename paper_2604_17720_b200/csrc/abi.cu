@@ -458,8 +458,9 @@ int run_grid(int dtype, const void* xyz, int64_t batch, int64_t cloud_stride, in
   // (KM = 32 — the kernel template supports it for 1-2 CTAs — was measured
   // slower at C5: 21 winners per round but 20K cycles per round.)
   int km = cl <= 2 ? 16 : 8;
-  if (const char* v = getenv("FFPS_GRID_KM"))
+  if (const char* v = getenv("FFPS_GRID_KM")) {
     if (atoi(v) == 8) km = 8;
+  }
   int64_t nb = 0;
   size_t smem = 0;
   for (int ppl = 1; ppl <= 8 && !pick; ppl *= 2) {

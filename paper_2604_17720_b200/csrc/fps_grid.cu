@@ -15,14 +15,14 @@ const GridInst* grid_instances_f32(int* count) {
 }
 
 const GridInst* grid_instances(int* count) {
-  static GridInst all[64];
+  static GridInst all[128];
   static int n = 0;
   static bool done = false;
   if (!done) {  // first call happens under the C ABI's plan (single-threaded init)
     for (auto get : {grid_instances_f32, grid_instances_f64, grid_instances_mixed}) {
       int c = 0;
       const GridInst* g = get(&c);
-      for (int i = 0; i < c && n < 64; ++i) all[n++] = g[i];
+      for (int i = 0; i < c && n < 128; ++i) all[n++] = g[i];
     }
     done = true;
   }

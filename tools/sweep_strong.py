@@ -54,7 +54,7 @@ def main():
             ref = None
             for sc in a.scheds:
                 name, _, km = sc.partition("/km")
-                os.environ.pop("FFPS_GRID_KM", None)
+                keep = os.environ.get("FFPS_GRID_KM")
                 if km:
                     os.environ["FFPS_GRID_KM"] = km
                 _device.set_schedule(name)
@@ -69,7 +69,10 @@ def main():
                                   "ms": round(ms, 3), "rounds": rounds,
                                   "cycles_per_round": round(cyc / max(rounds, 1), 1),
                                   "same": same}), flush=True)
-            os.environ.pop("FFPS_GRID_KM", None)
+                if km:
+                    os.environ.pop("FFPS_GRID_KM", None)
+                    if keep is not None:
+                        os.environ["FFPS_GRID_KM"] = keep
             _device.set_schedule("auto")
 
 
