@@ -44,8 +44,10 @@ def main():
     import argparse
     ap = argparse.ArgumentParser()
     ap.add_argument("clouds", nargs="*", default=["uniform"])
-    ap.add_argument("--scheds", nargs="*", default=["auto", "bucket", "grid", "stream"])
+    ap.add_argument("--scheds", nargs="*", default=["auto", "stream"])
     ap.add_argument("--configs", nargs="*", default=None, help="name prefixes, e.g. C5")
+    ap.add_argument("--precision", choices=["f64", "f32"], default="f64",
+                    help="f64: the reference's binary64 on the fp32 clouds (FFPS_F32_F64)")
     a = ap.parse_args()
     for kind in a.clouds:
         for name, B, N, budgets, ps in CONFIGS:
@@ -59,13 +61,15 @@ def main():
                 try:
                     heavy = N >= 100000 and sched in ("stream", "bucket")
                     ex = timeit(lambda: ffps.hierarchical_sample_batch(
-                        x, budgets, ffps.PruneConfig(p=0.0), 0, False),
+                        x, budgets, ffps.PruneConfig(p=0.0), 0, False, precision=a.precision),
                         1 if heavy else 2, 3 if heavy else 5)
                     rec = {"config": name, "cloud": kind, "B": B, "N": N, "schedule": sched,
+                           "precision": a.precision,
                            "exhaustive_ms": ex, "exhaustive_clouds_per_s": B / ex * 1e3}
                     for p in ps:
                         fl = timeit(lambda: ffps.hierarchical_sample_batch(
-                            x, budgets, ffps.PruneConfig(p=p), 0, True), 2, 5)
+                            x, budgets, ffps.PruneConfig(p=p), 0, True, precision=a.precision),
+                            2, 5)
                         k = ffps.PruneConfig(p=p).kernel_budget(budgets[0])
                         rec[f"flash_p{p}_ms"] = fl
                         rec[f"flash_p{p}_clouds_per_s"] = B / fl * 1e3
