@@ -47,6 +47,7 @@ BUDGETS = {200_000: (50_000, 12_500, 3_125, 781), 300_000: (75_000, 18_750, 4_68
            100_000: (25_000, 6_250, 1_562, 390), 24_000: (6_000, 1_500, 375, 93)}
 BYTES_PER_UNIT = {"f32": 20, "f64": 40}  # xyz read + dist read + dist write
 METRIC = "4-stage FPS clouds/sec at N=200K (FPS-Prune p=0.75 + FPS-Cache)"
+PREC_CODE = {"f32": 0, "f64": 2}   # ABI dtype of the fp32 clouds: binary32 / FFPS_F32_F64
 
 
 def parse(argv=None):
@@ -474,7 +475,8 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         ex_step, ex_kern = arm(cfg_exh, False, "auto", ks)
         exh = {"value": global_batch / (ex_step / 1e3), "unit": "clouds/s",
                "ms_per_step": ex_step, "ms_per_cloud": ex_step / B, "steps": ks,
-               "dtype": prec, "schedule": "auto (" + _native.auto_schedule(args.n, B) + ")",
+               "dtype": prec,
+               "schedule": "auto (" + _native.auto_schedule(args.n, B, PREC_CODE[prec]) + ")",
                "stage1_kernel_ms": float(np.mean([k[3] for k in ex_kern if k[1] == args.n])),
                "units_per_step": ex_units,
                "speedup_flash_vs_exhaustive": ex_step / ms_step}
@@ -592,7 +594,7 @@ def latency_roofline(args, x, budgets, cfg_flash, prec, kern, clocks, B) -> dict
     import paper_2604_17720_b200 as ffps
     from paper_2604_17720_b200 import _device, _native
     c1, k1 = stage_units(args.n, budgets, args.p, True)[0]
-    sched = _native.auto_schedule(c1, B)
+    sched = _native.auto_schedule(c1, B, PREC_CODE[prec])
     with _device.grid_stats() as gs:
         ffps.hierarchical_sample_batch(x, budgets, cfg_flash, 0, True, precision=prec)
     torch.cuda.synchronize()

@@ -99,11 +99,12 @@ int ffps_run_kernel(int dtype, const void* xyz, int64_t batch,
  *   FFPS_ALGO_SMALL   K1s: clouds of up to 8192 points, one CTA per cloud, points in
  *                     registers, one barrier per greedy step (larger clouds fall
  *                     back to STREAM);
- *   FFPS_ALGO_AUTO    GRID for n >= 16384 (any batch) or n >= 12288 with >= 16
- *                     clouds, 2 CTAs per cloud from n >= 20000 while the
- *                     batch fits the SMs twice; BUCKET for smaller clouds when
- *                     the batch fills the GPU; SMALL for n <= 8192; else
- *                     STREAM (the environment variable
+ *   FFPS_ALGO_AUTO    binary32: SMALL for n <= 8192, GRID from n >= 10000
+ *                     (2 CTAs per cloud from n >= 20000 while the batch fits
+ *                     the SMs twice), BUCKET for smaller clouds when the batch
+ *                     fills the GPU, else STREAM; binary64: SMALL up to 4608
+ *                     points, GRID on 1 CTA below 16384, GRID beyond (the
+ *                     environment variable
  *                     FFPS_ALGO=stream|small|bucket|grid overrides
  *                     AUTO). */
 enum ffps_algo { FFPS_ALGO_AUTO = 0, FFPS_ALGO_STREAM = 1, FFPS_ALGO_BUCKET = 2,
@@ -137,7 +138,10 @@ int ffps_h2d_prefix(void* dst, const void* src_host, int64_t batch, int64_t n_pr
  * (FFPS_ALGO_STREAM, FFPS_ALGO_BUCKET or FFPS_ALGO_GRID_CL(c) with the
  * cluster size chosen for the whole batch); callers that split one batch into
  * concurrent chunks decide once for the whole batch and pass the result. */
-int ffps_auto_schedule(int64_t n, int64_t batch);
+int ffps_auto_schedule(int64_t n, int64_t batch);  /* binary32 arithmetic */
+/* The same for the arithmetic of `dtype` (binary64 prefers the multi-winner
+ * schedule from 4,609 points on, binary32 from 10,000). */
+int ffps_auto_schedule_ex(int64_t n, int64_t batch, int dtype);
 
 /* ffps_run_kernel with an explicit schedule (same arguments; algo as above). */
 int ffps_run_kernel_ex(int dtype, const void* xyz, int64_t batch,

@@ -54,6 +54,7 @@ SIGNATURES = {
     "ffps_plan": (_int, [_int, _i64, _i64, ctypes.POINTER(_i64)]),
     "ffps_bucket_plan": (_int, [_int, _i64, ctypes.POINTER(_i64)]),
     "ffps_auto_schedule": (_int, [_i64, _i64]),
+    "ffps_auto_schedule_ex": (_int, [_i64, _i64, _int]),
     "ffps_h2d_prefix": (_int, [_vp, _vp, _i64, _i64, _i64, _int, _vp]),
     "ffps_last_launch_count": (_i64, []),
     "ffps_last_error": (ctypes.c_char_p, []),
@@ -174,11 +175,12 @@ def bucket_plan(dtype: int, n: int) -> dict:
     return dict(zip(keys, (int(v) for v in out)))
 
 
-def auto_schedule(n: int, batch: int) -> str:
-    """The schedule AUTO picks for a whole batch ("stream", "bucket" or
-    "grid@c", c = CTAs per cloud chosen for the whole batch)."""
+def auto_schedule(n: int, batch: int, dtype: int = F32) -> str:
+    """The schedule AUTO picks for a whole batch ("small", "stream", "bucket"
+    or "grid@c", c = CTAs per cloud chosen for the whole batch) under the
+    arithmetic of ``dtype`` (F32, F64 or F32_F64)."""
     names = {v: k for k, v in ALGO.items()}
-    return names[int(load().ffps_auto_schedule(n, batch))]
+    return names[int(load().ffps_auto_schedule_ex(n, batch, dtype))]
 
 
 def h2d_prefix(dst, src_host, batch, n_prefix, cloud_stride, dtype, stream) -> None:

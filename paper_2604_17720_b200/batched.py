@@ -395,7 +395,8 @@ def hierarchical_sample_host(points, budgets: Sequence[int], cfg: PruneConfig, s
     from . import _native
     sched = _device.current_schedule()
     if sched == "auto":
-        sched = _native.auto_schedule(c, B)
+        sched = _native.auto_schedule(c, B, _device.dtype_code(
+            host, torch.empty(0, dtype=_out_dtype(host, precision))))
     prev = _device.set_schedule(sched)
     try:
         main = torch.cuda.current_stream(dev)

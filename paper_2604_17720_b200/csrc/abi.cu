@@ -709,28 +709,36 @@ int run_streaming(int dtype, const void* xyz, int64_t batch, int64_t cloud_strid
   return FFPS_OK;
 }
 
-// FFPS_ALGO_AUTO (measured on B200 over batch 1..128 x n 8K..200K with
-// iters = n/4, tools/sweep_cl.py --grid, profiles/r01_sweep_cl.jsonl; the time
-// per cloud is flat in the batch until the clusters outnumber the SMs):
-//   GRID   (multi-winner rounds, bucket-group index) for clouds of >= 16K
-//          points, and >= 12K points once >= 16 clouds;
-//   BUCKET (one CTA per cloud, exact bucket bounds) for smaller clouds when the
-//          batch fills the GPU (>= 48 clouds of >= 6K points, >= 96 of >= 3K);
-//   SMALL  (one CTA per cloud, points in registers) for clouds of <= 8192
-//          points (tools/sweep_small.py, tools/sweep_stream_small.py);
-//   STREAM (clusters of up to 16 CTAs, every point every iteration) otherwise.
-// FFPS_ALGO in the environment ("stream" / "small" / "bucket" / "multi" /
-// "grid") overrides AUTO.
+// FFPS_ALGO_AUTO (measured on B200 over batch 1..64 x n 1K..200K with
+// iters = n/4, tools/sweep_auto.py / sweep_cl.py, profiles/r01_sweep_cl.jsonl,
+// profiles/r02_sweep_auto_f32.jsonl, r02_sweep_auto_f64.jsonl; the time per
+// cloud is flat in the batch until the clusters outnumber the SMs):
+// binary32 —
+//   SMALL  (one CTA per cloud, points in registers) for clouds of <= 8192 points;
+//   GRID   (multi-winner rounds, bucket-group index) from 10,000 points (12K:
+//          1 CTA per cloud 2.03-2.17 ms vs 2.25-3.7 for the others);
+//   BUCKET for 6K+ clouds when the batch fills the GPU, else STREAM;
+// binary64 (FFPS_F64, FFPS_F32_F64) —
+//   SMALL  up to 4,608 points (4K: 0.82 ms vs 1.31 on GRID@1);
+//   GRID on 1 CTA per cloud below 16K points (6K: 1.49-1.59 ms vs 1.94 on
+//          SMALL; 8K: 1.73-1.84 vs 4.7), GRID beyond.
+// FFPS_ALGO in the environment ("stream" / "small" / "bucket" / "grid")
+// overrides AUTO.
 constexpr int64_t kSmallMax = 8192;  // K1s: points per cloud at most
 
-int auto_algo(int64_t n, int64_t batch) {
-  if (n <= kSmallMax) return FFPS_ALGO_SMALL;  // tools/sweep_small.py: 1.2-2x the others
-  if (n >= 16384 || (n >= 12288 && batch >= 16)) return FFPS_ALGO_GRID;
+int auto_algo(int64_t n, int64_t batch, int dtype) {
+  if (dtype != FFPS_F32) {
+    if (n <= 4608) return FFPS_ALGO_SMALL;
+    if (n < 16384) return FFPS_ALGO_GRID_CL(1);
+    return FFPS_ALGO_GRID;
+  }
+  if (n <= kSmallMax) return FFPS_ALGO_SMALL;
+  if (n >= 10000) return FFPS_ALGO_GRID;
   if ((n >= 6144 && batch >= 48) || (n >= 3072 && batch >= 96)) return FFPS_ALGO_BUCKET;
   return FFPS_ALGO_STREAM;
 }
 
-int resolve_algo(int algo, int64_t n, int64_t batch) {
+int resolve_algo(int algo, int64_t n, int64_t batch, int dtype) {
   if (algo == FFPS_ALGO_AUTO) {
     const char* force = getenv("FFPS_FORCE_PLAN");  // names a streaming configuration
     if (force && *force) return FFPS_ALGO_STREAM;
@@ -740,7 +748,7 @@ int resolve_algo(int algo, int64_t n, int64_t batch) {
     if (env && strcmp(env, "multi") == 0) return FFPS_ALGO_GRID;  // retired K1m: K1g
     if (env && strcmp(env, "grid") == 0) return FFPS_ALGO_GRID;
     if (env && strcmp(env, "small") == 0) return FFPS_ALGO_SMALL;
-    return auto_algo(n, batch);
+    return auto_algo(n, batch, dtype);
   }
   return algo;
 }
@@ -798,15 +806,19 @@ int ffps_h2d_prefix(void* dst, const void* src_host, int64_t batch, int64_t n_pr
   return FFPS_OK;
 }
 
-int ffps_auto_schedule(int64_t n, int64_t batch) {
-  const int a = resolve_algo(FFPS_ALGO_AUTO, n, batch);
-  if (a != FFPS_ALGO_GRID) return a;
+int ffps_auto_schedule_ex(int64_t n, int64_t batch, int dtype) {
+  const int a = resolve_algo(FFPS_ALGO_AUTO, n, batch, dtype);
+  if ((a & 0xff) != FFPS_ALGO_GRID) return a;
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) {
     cudaGetLastError();
     return a;
   }
   return FFPS_ALGO_GRID_CL(grid_cluster(a, batch, device_info(dev).sms, n));
+}
+
+int ffps_auto_schedule(int64_t n, int64_t batch) {
+  return ffps_auto_schedule_ex(n, batch, FFPS_F32);
 }
 
 }  // extern "C"
@@ -897,7 +909,7 @@ int run_kernel_impl(int dtype, const void* xyz, int64_t batch, int64_t cloud_str
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
   // FFPS_ALGO_MULTI (K1m, retired in round 2) runs the multi-winner K1g
-  const int a = resolve_algo(algo == FFPS_ALGO_MULTI ? FFPS_ALGO_GRID : algo, n, batch);
+  const int a = resolve_algo(algo == FFPS_ALGO_MULTI ? FFPS_ALGO_GRID : algo, n, batch, dtype);
   return dispatch(dtype, xyz, batch, cloud_stride, n, iters, seed_pos, index_map, map_stride,
                   order, sel_d2, out_stride, static_cast<cudaStream_t>(stream), dev, a,
                   algo == FFPS_ALGO_AUTO, stats);
