@@ -134,6 +134,14 @@ int ffps_run_kernel_stats(int dtype, const void* xyz, int64_t batch,
 int ffps_h2d_prefix(void* dst, const void* src_host, int64_t batch, int64_t n_prefix,
                     int64_t cloud_stride, int dtype, void* stream);
 
+/* Device -> host copy of the first n_prefix elements (elem_bytes each) of
+ * every row of a [batch][src_stride] device array into a [batch][dst_stride]
+ * (pinned) host array, one pitched copy, stream-ordered: the greedy part of
+ * the selection distances (the fill's are 0 by definition,
+ * fps_prune.py:104-105, and are written on the host). */
+int ffps_d2h_prefix(void* dst_host, int64_t dst_stride, const void* src, int64_t src_stride,
+                    int64_t batch, int64_t n_prefix, int64_t elem_bytes, void* stream);
+
 /* The schedule FFPS_ALGO_AUTO picks for a batch of `batch` clouds of n points
  * (FFPS_ALGO_STREAM, FFPS_ALGO_BUCKET or FFPS_ALGO_GRID_CL(c) with the
  * cluster size chosen for the whole batch); callers that split one batch into

@@ -56,6 +56,7 @@ SIGNATURES = {
     "ffps_auto_schedule": (_int, [_i64, _i64]),
     "ffps_auto_schedule_ex": (_int, [_i64, _i64, _int]),
     "ffps_h2d_prefix": (_int, [_vp, _vp, _i64, _i64, _i64, _int, _vp]),
+    "ffps_d2h_prefix": (_int, [_vp, _i64, _vp, _i64, _i64, _i64, _i64, _vp]),
     "ffps_last_launch_count": (_i64, []),
     "ffps_last_error": (ctypes.c_char_p, []),
     "ffps_abi_version": (_int, []),
@@ -186,3 +187,9 @@ def auto_schedule(n: int, batch: int, dtype: int = F32) -> str:
 def h2d_prefix(dst, src_host, batch, n_prefix, cloud_stride, dtype, stream) -> None:
     check(load().ffps_h2d_prefix(dst, src_host, batch, n_prefix, cloud_stride, dtype, stream),
           "ffps_h2d_prefix")
+
+
+def d2h_prefix(dst_host, dst_stride, src, src_stride, batch, n_prefix, elem_bytes,
+               stream) -> None:
+    check(load().ffps_d2h_prefix(dst_host, dst_stride, src, src_stride, batch, n_prefix,
+                                 elem_bytes, stream), "ffps_d2h_prefix")

@@ -421,12 +421,22 @@ def hierarchical_sample_host(points, budgets: Sequence[int], cfg: PruneConfig, s
                 l1, stats1 = _fps_prune_device(x, b[0], cfg, seeds[lo:up], n=N,
                                                precision=precision)
                 hi[lo:up].copy_(l1.indices, non_blocking=pinned)
-                hs[lo:up].copy_(l1.selection_dist2, non_blocking=pinned)
+                # the fill's selection distances are 0 by definition
+                # (fps_prune.py:104-105): only the greedy part crosses PCIe
+                if pinned:   # one pitched copy into the strided pinned rows
+                    sd = l1.selection_dist2
+                    _native.d2h_prefix(hs[lo:up].data_ptr(), hs.stride(0), sd.data_ptr(),
+                                       sd.stride(0), up - lo, k, sd.element_size(),
+                                       st.cuda_stream)
+                else:
+                    hs[lo:up, :k].copy_(l1.selection_dist2[:, :k])
         for st in streams:
             if st is not main:
                 main.wait_stream(st)
     finally:
         _device.set_schedule(prev)
+    if b[0] > k:
+        hs[:, k:].zero_()   # on the host while the device works
     main.synchronize()
     stats1.cache_bytes = cache_footprint_bytes(b[0])
     res = [(hi[:, :m], hs[:, :m], min(k, m)) for m in b]

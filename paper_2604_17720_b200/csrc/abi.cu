@@ -806,6 +806,22 @@ int ffps_h2d_prefix(void* dst, const void* src_host, int64_t batch, int64_t n_pr
   return FFPS_OK;
 }
 
+int ffps_d2h_prefix(void* dst_host, int64_t dst_stride, const void* src, int64_t src_stride,
+                    int64_t batch, int64_t n_prefix, int64_t elem_bytes, void* stream) {
+  g_last_launches = 0;
+  if (batch < 0 || n_prefix < 0 || elem_bytes < 1 || dst_stride < n_prefix ||
+      src_stride < n_prefix)
+    return fail(FFPS_EINVAL, "d2h_prefix: bad arguments");
+  if (batch == 0 || n_prefix == 0) return FFPS_OK;
+  if (!dst_host || !src) return fail(FFPS_EINVAL, "null pointer");
+  cudaError_t e = cudaMemcpy2DAsync(dst_host, (size_t)(dst_stride * elem_bytes), src,
+                                    (size_t)(src_stride * elem_bytes),
+                                    (size_t)(n_prefix * elem_bytes), (size_t)batch,
+                                    cudaMemcpyDeviceToHost, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpy2DAsync");
+  return FFPS_OK;
+}
+
 int ffps_auto_schedule_ex(int64_t n, int64_t batch, int dtype) {
   const int a = resolve_algo(FFPS_ALGO_AUTO, n, batch, dtype);
   if ((a & 0xff) != FFPS_ALGO_GRID) return a;
