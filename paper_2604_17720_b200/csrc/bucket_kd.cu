@@ -318,23 +318,33 @@ __global__ void __launch_bounds__(kThreads, 1) bucket_kd_kernel(const BucketBuil
     }
     for (int i = tid; i < S * kBins1; i += kThreads) hist[i] = 0u;
     __syncthreads();
-    // histogram pass (segment-major: the whole CTA on one segment at a time)
-    for (int s = 0; s < S; ++s) {
+    // Warp groups: G segments at a time, one per group of kNW / G warps per
+    // rank (G = the largest power of two <= min(S, 8)); group wg takes
+    // segments wg, wg + G, ...  Deep levels have many small segments, which
+    // the whole CTA would walk one by one with most lanes idle.  Both passes
+    // use the same point -> thread mapping (gtid_g), so each rank's partial
+    // histogram counts exactly the points that rank places.
+    const int G = S >= 8 ? 8 : (S >= 4 ? 4 : (S >= 2 ? 2 : 1));
+    const int wg = warp % G;
+    const int GTg = GT / G;
+    const int gtid_g = ((rank * kNW + warp) / G) * 32 + lane;
+    // histogram pass (segment-major within each warp group)
+    for (int s = wg; s < S; s += G) {
       if (s_m[s] <= bs) continue;
       const int st = s_start[s], m = s_m[s], ax = s_ax[s];
       const T lo = s_lo[s], inv = s_inv[s];
       const T* v = ax == 0 ? src.x : (ax == 1 ? src.y : src.z);
       uint32_t* h = hist + s * kBins1;
-      for (int i0 = 0; i0 < m; i0 += GT * kU) {  // kU loads in flight, then the atomics
+      for (int i0 = 0; i0 < m; i0 += GTg * kU) {  // kU loads in flight, then the atomics
         T w[kU];
 #pragma unroll
         for (int u = 0; u < kU; ++u) {
-          const int i = i0 + u * GT + gtid;
+          const int i = i0 + u * GTg + gtid_g;
           w[u] = i < m ? v[st + i] : T(0);
         }
 #pragma unroll
         for (int u = 0; u < kU; ++u)
-          if (i0 + u * GT + gtid < m) atomicAdd(&h[haddr<kBins1>(bin_of<kBins1>(w[u], lo, inv))], 1u);
+          if (i0 + u * GTg + gtid_g < m) atomicAdd(&h[haddr<kBins1>(bin_of<kBins1>(w[u], lo, inv))], 1u);
       }
     }
     // CL > 1: each rank keeps its partial histogram (first half of `hist`,
@@ -385,8 +395,8 @@ __global__ void __launch_bounds__(kThreads, 1) bucket_kd_kernel(const BucketBuil
       }
     }
     __syncthreads();
-    // partition pass + children boxes
-    for (int s = 0; s < S; ++s) {
+    // partition pass + children boxes (the same warp groups)
+    for (int s = wg; s < S; s += G) {
       const int st = s_start[s], m = s_m[s];
       const bool split = m > bs;
       const int ax = s_ax[s], bstar = split ? s_b[s] : 0;
@@ -401,12 +411,12 @@ __global__ void __launch_bounds__(kThreads, 1) bucket_kd_kernel(const BucketBuil
           a[k][c] = pinf;
           z[k][c] = -pinf;
         }
-      for (int j0 = 0; j0 < m; j0 += GT * kU) {  // warp-uniform trip count
+      for (int j0 = 0; j0 < m; j0 += GTg * kU) {  // warp-uniform trip count
        T vv[kU][3];
        int32_t oo[kU];
 #pragma unroll
        for (int u = 0; u < kU; ++u) {  // kU points per thread in flight
-         const int i = j0 + u * GT + gtid;
+         const int i = j0 + u * GTg + gtid_g;
          const bool live = i < m;
          vv[u][0] = live ? src.x[st + i] : T(0);
          vv[u][1] = live ? src.y[st + i] : T(0);
@@ -415,7 +425,7 @@ __global__ void __launch_bounds__(kThreads, 1) bucket_kd_kernel(const BucketBuil
        }
 #pragma unroll
        for (int u = 0; u < kU; ++u) {
-        const int i = j0 + u * GT + gtid;
+        const int i = j0 + u * GTg + gtid_g;
         const bool live = i < m;
         const T v[3] = {vv[u][0], vv[u][1], vv[u][2]};
         const int32_t o = oo[u];
