@@ -1,5 +1,6 @@
 #!/bin/bash
-cd "$GRAFT_REPO_ROOT" || exit 1
+# iteration loop: parity of every GPU schedule suite that the kernels touch,
+# C5 greedy timings (64 and 16 clouds) and an ncu launch list of one C5 stage
 mkdir -p gpurun_out
 T=${1:-k0}
 {
