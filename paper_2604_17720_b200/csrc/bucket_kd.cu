@@ -43,9 +43,9 @@ namespace {
 
 constexpr int kThreads = 1024;
 constexpr int kNW = kThreads / 32;
-constexpr int kBins1 = 512;    // CTA phase: bins per segment histogram
+constexpr int kBins1 = 256;    // CTA phase: bins per segment histogram
 constexpr int kBinsL = 256;    // leaf kernel: bins per warp histogram
-constexpr int kMaxSeg = 64;    // CTA phase stops at this many segments
+constexpr int kMaxSeg = 128;   // CTA phase stops at this many segments
 constexpr int kStack = 24;
 constexpr int kU = 4;          // CTA phase: points per thread in flight     // per-warp DFS stack (depth <= log2(n / BS) + 1)
 
@@ -200,6 +200,7 @@ __global__ void __launch_bounds__(kThreads, 1) bucket_kd_kernel(const BucketBuil
   __shared__ I s_box[kMaxSeg][6];       // boxes of the current segments
   __shared__ I s_cbox[2 * kMaxSeg][6];  // boxes of their children
   __shared__ int s_S;
+  __shared__ int n_start[kMaxSeg], n_m[kMaxSeg], n_from[kMaxSeg], s_nidx[kMaxSeg];
 
   static_assert(CL == 1 || CL == 2, "1 or 2 CTAs per cloud");
   constexpr int GT = CL * kThreads;  // threads per cloud
@@ -502,31 +503,48 @@ __global__ void __launch_bounds__(kThreads, 1) bucket_kd_kernel(const BucketBuil
       }
     }
     __syncthreads();
-    // next level's segment list (children in order; unsplit segments carried)
-    if (tid == 0) {
-      int ns = 0;
-      int st2[kMaxSeg], m2[kMaxSeg], from[kMaxSeg];
-      for (int s = 0; s < S; ++s) {
-        if (s_m[s] > bs) {
-          st2[ns] = s_start[s];
-          m2[ns] = s_nl[s];
-          from[ns++] = 2 * s;
-          st2[ns] = s_start[s] + s_nl[s];
-          m2[ns] = s_m[s] - s_nl[s];
-          from[ns++] = 2 * s + 1;
-        } else {
-          st2[ns] = s_start[s];
-          m2[ns] = s_m[s];
-          from[ns++] = 2 * s;
+    // next level's segment list (children in order; unsplit segments carried):
+    // warp 0 scans the children counts (S <= kMaxSeg / 2 = 64: two per lane),
+    // then one thread per segment writes its children, one per child copies
+    if (warp == 0) {
+      const int c0 = lane < S ? (s_m[lane] > bs ? 2 : 1) : 0;
+      const int c1 = lane + 32 < S ? (s_m[lane + 32] > bs ? 2 : 1) : 0;
+      int p0 = c0, p1 = c1;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int a0 = __shfl_up_sync(0xffffffffu, p0, o), a1 = __shfl_up_sync(0xffffffffu, p1, o);
+        if (lane >= o) {
+          p0 += a0;
+          p1 += a1;
         }
       }
-      for (int s = 0; s < ns; ++s) {
-        s_start[s] = st2[s];
-        s_m[s] = m2[s];
-#pragma unroll
-        for (int c = 0; c < 6; ++c) s_box[s][c] = s_cbox[from[s]][c];
+      const int t0 = __shfl_sync(0xffffffffu, p0, 31);
+      if (lane < S) s_nidx[lane] = p0 - c0;
+      if (lane + 32 < S) s_nidx[lane + 32] = t0 + p1 - c1;
+      if (lane == 31) s_S = t0 + p1;
+    }
+    __syncthreads();
+    if (tid < S) {
+      const int s = tid, o = s_nidx[s];
+      if (s_m[s] > bs) {
+        n_start[o] = s_start[s];
+        n_m[o] = s_nl[s];
+        n_from[o] = 2 * s;
+        n_start[o + 1] = s_start[s] + s_nl[s];
+        n_m[o + 1] = s_m[s] - s_nl[s];
+        n_from[o + 1] = 2 * s + 1;
+      } else {
+        n_start[o] = s_start[s];
+        n_m[o] = s_m[s];
+        n_from[o] = 2 * s;
       }
-      s_S = ns;
+    }
+    __syncthreads();
+    if (tid < s_S) {
+      s_start[tid] = n_start[tid];
+      s_m[tid] = n_m[tid];
+#pragma unroll
+      for (int c = 0; c < 6; ++c) s_box[tid][c] = s_cbox[n_from[tid]][c];
     }
     par ^= 1;
     __syncthreads();
@@ -557,7 +575,7 @@ __global__ void __launch_bounds__(kThreads, 1) bucket_kd_kernel(const BucketBuil
 // and — for the last bucket — the padding slots (first point of the bucket,
 // D = -inf, O = -1).
 template <typename T>
-__global__ void __launch_bounds__(256) bucket_kd_leaves_kernel(const BucketBuildParams p,
+__global__ void __launch_bounds__(512) bucket_kd_leaves_kernel(const BucketBuildParams p,
                                                                const int32_t* seg_hdr,
                                                                const int32_t* seg_sm,
                                                                const T* seg_box, int cap,
@@ -839,8 +857,8 @@ cudaError_t launch_bucket_kd(int dtype, const BucketBuildParams& p, int64_t batc
   // leaf kernel: up to 4 warps (segments) per CTA with their segments staged
   // in shared memory; 2 or 1 for bigger segments; global arrays beyond that
   const int mmax = kd_max_segment(p.n, p.bs);
-  int cap = (mmax + 31) / 32 * 32, wpc = 8;
-  while (wpc > 1 && (size_t)wpc * kd_leaves_warp_bytes(cap, esz) > (size_t)optin) wpc >>= 1;
+  int cap = (mmax + 31) / 32 * 32, wpc = 16;
+  while (wpc > 1 && (size_t)wpc * kd_leaves_warp_bytes(cap, esz) > (size_t)optin) --wpc;
   if ((size_t)wpc * kd_leaves_warp_bytes(cap, esz) > (size_t)optin) {
     cap = 0;
     wpc = 4;
