@@ -453,7 +453,9 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     e2e_val = global_batch / (e2e_step / 1e3)
     c1_, k1_ = stage_units(args.n, budgets, args.p, True)[0]
     h2d = B * c1_ * 3 * 4   # cache on: only the fp32 candidate prefix is read (fps_prune.py:92)
-    d2h = B * budgets[0] * (8 + out_s.element_size())
+    # int64 indices of layer 1 + the greedy part of its selection distances (the
+    # fill's are 0 by definition and are written on the host, fps_prune.py:104-105)
+    d2h = B * budgets[0] * 8 + B * k1_ * out_s.element_size()
 
     # exhaustive 4-stage arm of the same build (the paper's "standard CUDA FPS")
     exh = None
