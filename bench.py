@@ -587,16 +587,28 @@ def latency_roofline(args, x, budgets, cfg_flash, prec, kern, clocks, B) -> dict
     memory, the bucket SoA in L2), so bytes do not bound it: each greedy
     round is a dependent chain (flag -> re-evaluate -> rank -> DSMEM exchange
     -> chain test).  The bound is the latency of that chain.  Its floor is
-    measured live with the same kernel instance on a minimal table (one
-    bucket group per CTA, the same clusters per SM): peak = 1 / floor round
-    time.  achieved = the rounds of one C5 launch (kernel counters,
-    ffps_run_kernel_stats) / the greedy call's CUDA-event time (K0 bucket
-    build included, so frac is conservative)."""
+    measured live with the same kernel instance on the smallest table that
+    keeps the standard ranking path (16 bucket groups per CTA, the same
+    clusters per SM): peak = 1 / floor round time.  achieved = the rounds of
+    one C5 launch (kernel counters, ffps_run_kernel_stats) / the greedy
+    call's CUDA-event time (K0 bucket build included, so frac is
+    conservative).  Workloads whose greedy stage AUTO runs on another
+    schedule get the HBM-streaming comparison only."""
     import torch
     import paper_2604_17720_b200 as ffps
     from paper_2604_17720_b200 import _device, _native
     c1, k1 = stage_units(args.n, budgets, args.p, True)[0]
     sched = _native.auto_schedule(c1, B, PREC_CODE[prec])
+    kms = float(np.mean([k[3] for k in kern if k[1] == c1])) if kern else float("nan")
+    units = B * c1 * (k1 - 1)
+    if not sched.startswith("grid"):
+        gbs = units * BYTES_PER_UNIT[prec] / (kms / 1e3) / 1e9
+        pk = peaks()
+        return {"bound": "hbm", "achieved": gbs, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                "frac": gbs / pk["hbm_gbs"], "traffic": None, "kernel": sched,
+                "kernel_ms": kms, "peak_src": pk["src"],
+                "note": "greedy stage not on the multi-winner schedule: the standard "
+                        "streaming FPS's algorithmic bytes over the greedy call's time"}
     with _device.grid_stats() as gs:
         ffps.hierarchical_sample_batch(x, budgets, cfg_flash, 0, True, precision=prec)
     torch.cuda.synchronize()
@@ -625,11 +637,9 @@ def latency_roofline(args, x, budgets, cfg_flash, prec, kern, clocks, B) -> dict
     f_general = float(sf[:, 3].mean()) / cl
     floor_cpr = f_cycles / max(f_rounds, 1.0)
     cpr = cycles / max(rounds, 1.0)
-    kms = float(np.mean([k[3] for k in kern if k[1] == c1])) if kern else float("nan")
     sm_mhz = clocks.get("sm_mhz") or peaks()["sm_max_mhz"]
     peak = sm_mhz * 1e6 / floor_cpr                  # rounds/s per cloud at the floor
     achieved = rounds / (kms / 1e3)                  # rounds/s per cloud, event-timed
-    units = B * c1 * (k1 - 1)
     return {"bound": "latency", "achieved": achieved, "peak": peak,
             "unit": "greedy rounds/s per cloud", "frac": achieved / peak,
             "traffic": dram_traffic("fps_grid_kernel", prec),
