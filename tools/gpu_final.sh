@@ -16,4 +16,5 @@ for gb in 32 16 8; do
 done
 FFPS_BENCH_SHARE_GPU=1 timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29511 bench.py --gpus 2 --steps 3 --warmup 3 --no-cpu-baseline --no-extras --exh-steps 1 > gpurun_out/${T}_dist2.json 2> gpurun_out/${T}_dist2.err; echo "dist2=$?" >> gpurun_out/${T}_dist2.err
 timeout 2400 python tools/bench_configs.py uniform lidar > gpurun_out/${T}_configs.jsonl 2> gpurun_out/${T}_configs.err
+timeout 600 python bench.py --n 24000 --dtype f32 --global-batch 16 --no-exhaustive --no-extras --no-cpu-baseline > gpurun_out/${T}_bench_c2_f32.json 2>&1
 echo done
