@@ -453,11 +453,11 @@ int run_grid(int dtype, const void* xyz, int64_t batch, int64_t cloud_stride, in
   const ffps::GridInst* insts = ffps::grid_instances(&cnt);
   const ffps::GridInst* pick = nullptr;
   const int cl = grid_cluster(algo, batch, di.sms, n);  // CTAs per cloud
-  // winners per round at most: 16 with 1-2 CTAs per cloud (one DSMEM record
-  // per lane: CL * KM <= 32), 8 with 4 CTAs per cloud; FFPS_GRID_KM=8 forces 8.
+  // winners per round at most: 16 (one DSMEM record per lane with 1-2 CTAs per
+  // cloud, two per lane with 4); FFPS_GRID_KM=8 forces 8.
   // (KM = 32 — the kernel template supports it for 1-2 CTAs — was measured
   // slower at C5: 21 winners per round but 20K cycles per round.)
-  int km = cl <= 2 ? 16 : 8;
+  int km = 16;
   if (const char* v = getenv("FFPS_GRID_KM")) {
     if (atoi(v) == 8) km = 8;
   }
@@ -754,13 +754,22 @@ int resolve_algo(int algo, int64_t n, int64_t batch, int dtype) {
 }
 
 // CTAs per cloud of the grid schedule: fixed by the algo argument
-// (FFPS_ALGO_GRID_CL), else 2 for clouds of >= 20K points while batch * 2 <= SMs
-// (each CTA keeps >= 10 bucket groups for the KM = 16 candidates), else 1.
-// 4 CTAs per cloud (KM = 8) was never the fastest in the sweep (sweep_cl.py).
+// (FFPS_ALGO_GRID_CL), else
+//   4 for clouds of >= 48K points while batch * 4 <= SMs (each CTA still keeps
+//     >= 12K points; 75K: 9.2 vs 11.0 ms binary32, 10.8 vs 12.6 binary64;
+//     50K: 6.49 vs 6.67 / 7.60 vs 7.86; 37.5K: 5% slower, 25K: 12% slower —
+//     profiles/r02_ab_cl4_km16.txt, tools/sweep_strong.py),
+//   2 for clouds of >= 20K points while batch * 2 <= SMs (each CTA keeps
+//     >= 10 bucket groups for the KM = 16 candidates),
+//   else 1.
 // FFPS_GRID_CL in the environment overrides both.
 int grid_cluster(int algo, int64_t batch, int sms, int64_t n) {
   int cl = algo >> 8;
-  if (cl == 0) cl = (n >= 20000 && batch * 2 <= sms) ? 2 : 1;
+  if (cl == 0) {
+    if (n >= 48000 && batch * 4 <= sms) cl = 4;
+    else if (n >= 20000 && batch * 2 <= sms) cl = 2;
+    else cl = 1;
+  }
   if (const char* v = getenv("FFPS_GRID_CL")) {
     const int w = atoi(v);
     if (w == 1 || w == 2 || w == 4) cl = w;

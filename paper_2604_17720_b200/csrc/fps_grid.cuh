@@ -141,7 +141,8 @@ __host__ __device__ constexpr size_t grid_smem_bytes(int64_t nb) {
 
 // DSMEM record of a cluster rank's local top list (CL > 1), 32-bit words:
 // float  [v, pos, x, y, z, v2, q, flag]                     (8 words)
-// double [v lo, v hi, v2 lo, v2 hi, x, x, y, y, z, z, pos, q, flag, pad x3] (16)
+// double [v lo, v hi, v2 lo, v2 hi, x, x, y, y, z, z, pos, q | flag << 30] (12:
+//        three 16-byte stores; q < 2^30, read only from live records)
 template <typename T>
 struct GridRec;
 template <>
@@ -162,16 +163,16 @@ struct GridRec<float> {
 };
 template <>
 struct GridRec<double> {
-  static constexpr int W = 16;
+  static constexpr int W = 12;
 
   __device__ static void send(uint32_t dst, uint32_t bar, int64_t v, int64_t v2, uint32_t pos,
                               int q, double x, double y, double z, uint32_t flag) {
     st_async_v2_b64(dst, bar, (uint64_t)v, (uint64_t)v2);
     st_async_v2_b64(dst + 16, bar, (uint64_t)__double_as_longlong(x),
                     (uint64_t)__double_as_longlong(y));
+    const uint32_t qf = ((uint32_t)q & 0x3fffffffu) | (flag << 30);
     st_async_v2_b64(dst + 32, bar, (uint64_t)__double_as_longlong(z),
-                    (uint64_t)pos | ((uint64_t)(uint32_t)q << 32));
-    st_async_v2_b64(dst + 48, bar, (uint64_t)flag, 0ull);
+                    (uint64_t)pos | ((uint64_t)qf << 32));
   }
   __device__ static int64_t u64(const uint32_t* w, int i) {
     return (int64_t)(((uint64_t)w[2 * i + 1] << 32) | w[2 * i]);
@@ -179,8 +180,8 @@ struct GridRec<double> {
   __device__ static int64_t v(const uint32_t* w) { return u64(w, 0); }
   __device__ static int64_t v2(const uint32_t* w) { return u64(w, 1); }
   __device__ static uint32_t pos(const uint32_t* w) { return w[10]; }
-  __device__ static int q(const uint32_t* w) { return (int)w[11]; }
-  __device__ static uint32_t flag(const uint32_t* w) { return w[12]; }
+  __device__ static int q(const uint32_t* w) { return (int)(w[11] & 0x3fffffffu); }
+  __device__ static uint32_t flag(const uint32_t* w) { return w[11] >> 30; }
   __device__ static double c(const uint32_t* w, int i) { return __longlong_as_double(u64(w, 2 + i)); }
 };
 
@@ -204,8 +205,8 @@ __global__ void __launch_bounds__(NT, 1) fps_grid_kernel(const BucketParams prm)
 
   static_assert(CL == 1 || CL == 2 || CL == 4, "cluster of 1, 2 or 4 CTAs");
   static_assert(NW == kWppNW, "flag-phase table sized for 16 warps");
-  static_assert(CL * KM <= 32 || (CL == 2 && KM == 32),
-                "one exchanged record per lane, or two lists of 32 (half-cleaner in lane)");
+  static_assert(CL * KM <= 32 || (CL == 2 && KM == 32) || (CL == 4 && KM == 16),
+                "one exchanged record per lane, two lists of 32, or four lists of 16");
   using R = GridRec<T>;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int rank = CL > 1 ? (int)cluster_ctarank() : 0;
@@ -927,7 +928,59 @@ __global__ void __launch_bounds__(NT, 1) fps_grid_kernel(const BucketParams prm)
       int idx = -1;
       bits_t mv = A::kmin;
       uint32_t mp = kNoIdx;
-      if constexpr (CL * KM == 64) {
+      if constexpr (CL == 4 && KM == 16) {
+        // four lists of 16 in two slots (lists 0-1 | 2-3, lane l: element
+        // l % 16 of list l / 16 of its pair, odd lists reversed, so each slot
+        // is a bitonic 32).  Only the best KM = 16 of the 64 are used: one
+        // half-cleaner per slot (one shuffle: lanes 0-15 keep the better 16
+        // of slot a, lanes 16-31 those of slot b), four stages sorting lanes
+        // 0-15 descending and 16-31 ascending, a half-cleaner across them and
+        // four stages sorting the best 16 into lanes 0-15 (10 stages, not the
+        // 16 of a full 64-merge)
+        auto ld = [&](int list, int e, bits_t& v, uint32_t& p, int& ix) {
+          ix = list * KM + ((list & 1) ? KM - 1 - e : e);
+          v = R::v(rec + ix * R::W);
+          p = R::pos(rec + ix * R::W);
+        };
+        const bool hi = (lane & 16) != 0;
+        {
+          bits_t va, vb;
+          uint32_t pa, pb;
+          int ia, ib;
+          ld(lane / KM, lane % KM, va, pa, ia);
+          ld(2 + lane / KM, lane % KM, vb, pb, ib);
+          // lane l < 16 needs a[l ^ 16]; lane l >= 16 needs b[l ^ 16]
+          const bits_t ov = A::shfl(hi ? va : vb, lane ^ 16);
+          const uint32_t op = __shfl_sync(0xffffffffu, hi ? pa : pb, lane ^ 16);
+          const int oi = __shfl_sync(0xffffffffu, hi ? ia : ib, lane ^ 16);
+          mv = hi ? vb : va;
+          mp = hi ? pb : pa;
+          idx = hi ? ib : ia;
+          if (ov > mv || (ov == mv && op < mp)) {
+            mv = ov;
+            mp = op;
+            idx = oi;
+          }
+        }
+        auto st_dir = [&](int j, bool up) {  // up: the better one to the higher lane
+          const bits_t ov = __shfl_xor_sync(0xffffffffu, mv, j);
+          const uint32_t op = __shfl_xor_sync(0xffffffffu, mp, j);
+          const int oi = __shfl_xor_sync(0xffffffffu, idx, j);
+          const bool other_better = ov > mv || (ov == mv && op < mp);
+          const bool mine_better = mv > ov || (mv == ov && mp < op);
+          if (((lane & j) == 0) != up ? other_better : mine_better) {
+            mv = ov;
+            mp = op;
+            idx = oi;
+          }
+        };
+#pragma unroll
+        for (int j = 8; j > 0; j >>= 1) st_dir(j, hi);
+        st_dir(16, false);
+#pragma unroll
+        for (int j = 8; j > 0; j >>= 1) st_dir(j, false);
+      } else {
+      if constexpr (CL == 2 && KM == 32) {
         // two lists of 32: lane l compares element l of list 0 with element
         // 31 - l of list 1 (half-cleaner); the better 32 form a bitonic sequence
         const int ia = lane, ib = KM + KM - 1 - lane;
@@ -965,6 +1018,7 @@ __global__ void __launch_bounds__(NT, 1) fps_grid_kernel(const BucketParams prm)
         idx = __shfl_sync(0xffffffffu, idx, src);
 #pragma unroll
         for (int j = 2 * KM; j > 0; j >>= 1) stage(j);
+      }
       }
       // lane r now holds the r-th record; a truncated list is exact only up to
       // its one record (its head)

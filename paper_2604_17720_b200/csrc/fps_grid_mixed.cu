@@ -8,7 +8,7 @@ namespace ffps {
 const GridInst* grid_instances_mixed(int* count) {
   static const GridInst insts[] = {
       FFPS_GRID_PPL(double, float, 8, 1), FFPS_GRID_PPL(double, float, 8, 2), FFPS_GRID_PPL(double, float, 8, 4),
-      FFPS_GRID_PPL(double, float, 16, 1), FFPS_GRID_PPL(double, float, 16, 2),
+      FFPS_GRID_PPL(double, float, 16, 1), FFPS_GRID_PPL(double, float, 16, 2), FFPS_GRID_PPL(double, float, 16, 4),
   };
   *count = (int)(sizeof(insts) / sizeof(insts[0]));
   return insts;

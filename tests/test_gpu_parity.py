@@ -40,7 +40,7 @@ class _Sched:
             os.environ["FFPS_GRID_KM"] = self.prev_km
 
 
-SCHEDULES = ["stream", "small", "bucket", "grid", "grid@1", "grid@2", "grid@2/km8"]
+SCHEDULES = ["stream", "small", "bucket", "grid", "grid@1", "grid@2", "grid@4", "grid@2/km8"]
 
 
 @pytest.fixture(params=SCHEDULES)
@@ -279,6 +279,24 @@ def test_errors_raised_before_device_work(cuda):
         ffps.hierarchical_sample(cloud, (8, 2), ffps.PruneConfig())
 
 
+def test_auto_schedule_choices(cuda):
+    """AUTO's measured thresholds (abi.cu auto_algo / grid_cluster) on the
+    B200's SM count: 4 CTAs per cloud for >= 48K-point clouds while the
+    batch fits 4 per SM, else 2, else 1; small / stream / bucket below."""
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    F32, F64, MIX = _native.F32, _native.F64, _native.F32_F64
+    for dt in (F32, F64, MIX):
+        assert _native.auto_schedule(50_000, sms // 4, dt) == "grid@4"
+        assert _native.auto_schedule(50_000, sms // 4 + 1, dt) == "grid@2"
+        assert _native.auto_schedule(40_000, 8, dt) == "grid@2"
+        assert _native.auto_schedule(50_000, sms // 2 + 1, dt) == "grid@1"
+    assert _native.auto_schedule(4_000, 8, F64) == "small"
+    assert _native.auto_schedule(8_000, 8, F64) == "grid@1"
+    assert _native.auto_schedule(8_000, 8, F32) == "small"
+    assert _native.auto_schedule(9_000, 8, F32) == "stream"
+    assert _native.auto_schedule(9_000, 64, F32) == "bucket"
+
+
 def test_abi_rejects_bad_arguments(cuda):
     lib = _native.load()
     rc = lib.ffps_run_kernel(0, 1, 1, 10, 10, 11, 1, None, 0, 1, 1, 11, None)
@@ -289,7 +307,7 @@ def test_abi_rejects_bad_arguments(cuda):
 
 
 @pytest.mark.parametrize("sched", ["bucket", "grid@1", "grid@2", "grid@4", "grid@1/km8",
-                                   "grid@2/km8"])
+                                   "grid@2/km8", "grid@4/km8"])
 @pytest.mark.parametrize("dtype", [np.float32, np.float64])
 def test_bucketed_schedule_sizes_and_ties(cuda, dtype, sched):
     """K0+K1b / K1g forced on every size class: n below / at / above
@@ -306,7 +324,7 @@ def test_bucketed_schedule_sizes_and_ties(cuda, dtype, sched):
 
 
 @pytest.mark.parametrize("dtype", [np.float32, np.float64])
-@pytest.mark.parametrize("sched", ["grid@1", "grid@2", "grid@4", "grid@2/km8"])
+@pytest.mark.parametrize("sched", ["grid@1", "grid@2", "grid@4", "grid@2/km8", "grid@4/km8"])
 def test_multi_winner_degenerate_ties(cuda, dtype, sched):
     """K1g when hundreds of bucket keys tie (identical points, exhausted
     buckets): the candidate list overflows and rounds fall back to one exact
