@@ -755,10 +755,10 @@ int resolve_algo(int algo, int64_t n, int64_t batch, int dtype) {
 
 // CTAs per cloud of the grid schedule: fixed by the algo argument
 // (FFPS_ALGO_GRID_CL), else
-//   4 for clouds of >= 48K points while batch * 4 <= SMs (each CTA still keeps
-//     >= 12K points; 75K: 9.2 vs 11.0 ms binary32, 10.8 vs 12.6 binary64;
-//     50K: 6.49 vs 6.67 / 7.60 vs 7.86; 37.5K: 5% slower, 25K: 12% slower —
-//     profiles/r02_ab_cl4_km16.txt, tools/sweep_strong.py),
+//   4 for clouds of >= 40K points while batch * 4 <= SMs (crossover 37.5-42K:
+//     37.5K 1-2% slower, 42K 1-2% faster, 50K 5-7% faster, 75K 18-19% faster,
+//     binary32 and binary64 alike — profiles/r02_ab_cl4_crossover.txt,
+//     r02_ab_cl4_top16_merge.txt, tools/sweep_strong.py),
 //   2 for clouds of >= 20K points while batch * 2 <= SMs (each CTA keeps
 //     >= 10 bucket groups for the KM = 16 candidates),
 //   else 1.
@@ -766,7 +766,7 @@ int resolve_algo(int algo, int64_t n, int64_t batch, int dtype) {
 int grid_cluster(int algo, int64_t batch, int sms, int64_t n) {
   int cl = algo >> 8;
   if (cl == 0) {
-    if (n >= 48000 && batch * 4 <= sms) cl = 4;
+    if (n >= 40000 && batch * 4 <= sms) cl = 4;
     else if (n >= 20000 && batch * 2 <= sms) cl = 2;
     else cl = 1;
   }

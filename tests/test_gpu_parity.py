@@ -281,14 +281,15 @@ def test_errors_raised_before_device_work(cuda):
 
 def test_auto_schedule_choices(cuda):
     """AUTO's measured thresholds (abi.cu auto_algo / grid_cluster) on the
-    B200's SM count: 4 CTAs per cloud for >= 48K-point clouds while the
+    B200's SM count: 4 CTAs per cloud for >= 40K-point clouds while the
     batch fits 4 per SM, else 2, else 1; small / stream / bucket below."""
     sms = torch.cuda.get_device_properties(0).multi_processor_count
     F32, F64, MIX = _native.F32, _native.F64, _native.F32_F64
     for dt in (F32, F64, MIX):
         assert _native.auto_schedule(50_000, sms // 4, dt) == "grid@4"
         assert _native.auto_schedule(50_000, sms // 4 + 1, dt) == "grid@2"
-        assert _native.auto_schedule(40_000, 8, dt) == "grid@2"
+        assert _native.auto_schedule(40_000, 8, dt) == "grid@4"
+        assert _native.auto_schedule(39_999, 8, dt) == "grid@2"
         assert _native.auto_schedule(50_000, sms // 2 + 1, dt) == "grid@1"
     assert _native.auto_schedule(4_000, 8, F64) == "small"
     assert _native.auto_schedule(8_000, 8, F64) == "grid@1"
