@@ -94,8 +94,10 @@ int ffps_run_kernel(int dtype, const void* xyz, int64_t batch,
  *                     shared memory and indexed by groups of 32 (kd order), so
  *                     a selected point only tests the buckets within its reach;
  *                     each cloud's buckets are split over a cluster of 1, 2 or
- *                     4 CTAs: FFPS_ALGO_GRID_CL(c) fixes c, plain FFPS_ALGO_GRID
- *                     takes 2 for n >= 20000 while batch * 2 <= SM count, else 1;
+ *                     4 CTAs: FFPS_ALGO_GRID_CL(c) fixes c, plain
+ *                     FFPS_ALGO_GRID takes 4 for n >= 40000 while the batch's
+ *                     4-CTA clusters are all resident at once, else 2 for
+ *                     n >= 20000 while batch * 2 <= SM count, else 1;
  *   FFPS_ALGO_SMALL   K1s: clouds of up to 8192 points, one CTA per cloud, points in
  *                     registers, one barrier per greedy step (larger clouds fall
  *                     back to STREAM);

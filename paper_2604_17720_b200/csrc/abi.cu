@@ -444,30 +444,22 @@ int run_bucketed(int dtype, const void* xyz, int64_t batch, int64_t cloud_stride
 // K1g: smallest bucket size whose bucket table + cell index fit shared memory
 int grid_cluster(int algo, int64_t batch, int sms, int64_t n);
 
-int run_grid(int dtype, const void* xyz, int64_t batch, int64_t cloud_stride, int64_t n,
-             int64_t iters, const int64_t* seed_pos, const int64_t* index_map, int64_t map_stride,
-             int64_t* order, void* sel_d2, int64_t out_stride, cudaStream_t st, int dev,
-             int algo, int64_t* stats) {
-  const DeviceInfo di = device_info(dev);
+struct GridPick {
+  const ffps::GridInst* inst = nullptr;
+  int64_t nb = 0;   // buckets per cloud
+  size_t smem = 0;  // dynamic shared memory per CTA
+};
+
+// the smallest bucket size whose per-rank table fits shared memory
+GridPick pick_grid(int dtype, int64_t n, int cl, int km, const DeviceInfo& di) {
   int cnt = 0;
   const ffps::GridInst* insts = ffps::grid_instances(&cnt);
-  const ffps::GridInst* pick = nullptr;
-  const int cl = grid_cluster(algo, batch, di.sms, n);  // CTAs per cloud
-  // winners per round at most: 16 (one DSMEM record per lane with 1-2 CTAs per
-  // cloud, two per lane with 4); FFPS_GRID_KM=8 forces 8.
-  // (KM = 32 — the kernel template supports it for 1-2 CTAs — was measured
-  // slower at C5: 21 winners per round but 20K cycles per round.)
-  int km = 16;
-  if (const char* v = getenv("FFPS_GRID_KM")) {
-    if (atoi(v) == 8) km = 8;
-  }
-  int64_t nb = 0;
-  size_t smem = 0;
-  for (int ppl = 1; ppl <= 8 && !pick; ppl *= 2) {
-    nb = (n + 32 * ppl - 1) / (32 * ppl);
-    const int64_t nbl = (nb + cl - 1) / cl;  // buckets of cluster rank 0 (the most)
-    if (nbl > 4096) continue;                 // <= 128 bucket groups per CTA
-    smem = ffps::grid_smem(dtype, nbl);
+  GridPick g;
+  for (int ppl = 1; ppl <= 8 && !g.inst; ppl *= 2) {
+    g.nb = (n + 32 * ppl - 1) / (32 * ppl);
+    const int64_t nbl = (g.nb + cl - 1) / cl;  // buckets of cluster rank 0 (the most)
+    if (nbl > 4096) continue;                  // <= 128 bucket groups per CTA
+    g.smem = ffps::grid_smem(dtype, nbl);
     for (int i = 0; i < cnt; ++i)
       if (insts[i].dtype == dtype && insts[i].ppl == ppl && insts[i].km == km &&
           insts[i].cl == cl) {
@@ -476,9 +468,97 @@ int run_grid(int dtype, const void* xyz, int64_t batch, int64_t cloud_stride, in
           cudaGetLastError();
           continue;
         }
-        if (smem + fa.sharedSizeBytes <= di.smem_optin) pick = &insts[i];  // + static smem
+        if (g.smem + fa.sharedSizeBytes <= di.smem_optin) g.inst = &insts[i];  // + static smem
       }
   }
+  return g;
+}
+
+cudaError_t prepare_grid_fn(int dev, const void* fn) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  auto key = std::make_pair(dev, fn);
+  if (g_attr_done.count(key)) return cudaSuccess;
+  cudaFuncAttributes fa;
+  cudaError_t e = cudaFuncGetAttributes(&fa, fn);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)(device_info_nolock(dev).smem_optin - fa.sharedSizeBytes));
+  if (e == cudaSuccess) g_attr_done[key] = true;
+  return e;
+}
+
+// clusters of one K1g instance resident at once (one CTA per SM; a cluster
+// must fit in one GPC, so fewer 4-CTA clusters fit than SMs / 4: 33 to 35
+// on the B200, measured)
+int grid_max_clusters(int dev, const GridPick& g) {
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    auto it = g_occ.find(std::make_tuple(dev, g.inst->fn, g.inst->cl));
+    if (it != g_occ.end()) return it->second;
+  }
+  int result = 0;
+  if (prepare_grid_fn(dev, g.inst->fn) == cudaSuccess) {
+    cudaLaunchConfig_t cfg;
+    memset(&cfg, 0, sizeof cfg);
+    cfg.gridDim = dim3(g.inst->cl * 64, 1, 1);
+    cfg.blockDim = dim3(g.inst->nt, 1, 1);
+    cfg.dynamicSmemBytes = g.smem;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = g.inst->cl;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (cudaOccupancyMaxActiveClusters(&result, g.inst->fn, &cfg) != cudaSuccess) {
+      cudaGetLastError();
+      result = 0;
+    }
+  } else {
+    cudaGetLastError();
+  }
+  std::lock_guard<std::mutex> lk(g_mu);
+  g_occ[std::make_tuple(dev, g.inst->fn, g.inst->cl)] = result;
+  return result;
+}
+
+// K1g configuration of a batch: CTAs per cloud by grid_cluster; when AUTO
+// chose 4 and the batch's clusters would not all be resident at once (a
+// second wave doubles the time), halve it
+GridPick choose_grid(int dtype, int64_t n, int64_t batch, int algo, int dev, int* cl_out) {
+  const DeviceInfo di = device_info(dev);
+  const bool forced = (algo >> 8) != 0 || getenv("FFPS_GRID_CL") != nullptr;
+  int cl = grid_cluster(algo, batch, di.sms, n);
+  GridPick g;
+  for (;;) {
+    // winners per round at most: 16 (one DSMEM record per lane with 1-2 CTAs
+    // per cloud, two per lane with 4); FFPS_GRID_KM=8 forces 8.  (KM = 32 was
+    // measured slower at C5: 21 winners per round but 20K cycles per round,
+    // DESIGN.md.)
+    int km = 16;
+    if (const char* v = getenv("FFPS_GRID_KM")) {
+      if (atoi(v) == 8) km = 8;
+    }
+    g = pick_grid(dtype, n, cl, km, di);
+    if (!forced && cl > 2 && (!g.inst || grid_max_clusters(dev, g) < batch)) {
+      cl /= 2;
+      continue;
+    }
+    break;
+  }
+  *cl_out = cl;
+  return g;
+}
+
+int run_grid(int dtype, const void* xyz, int64_t batch, int64_t cloud_stride, int64_t n,
+             int64_t iters, const int64_t* seed_pos, const int64_t* index_map, int64_t map_stride,
+             int64_t* order, void* sel_d2, int64_t out_stride, cudaStream_t st, int dev,
+             int algo, int64_t* stats) {
+  int cl = 0;
+  const GridPick g = choose_grid(dtype, n, batch, algo, dev, &cl);
+  const ffps::GridInst* pick = g.inst;
+  const int64_t nb = g.nb;
+  const size_t smem = g.smem;
   if (!pick) return fail(FFPS_EUNSUPPORTED, "no grid configuration for n=%lld", (long long)n);
   const int64_t bs = 32 * pick->ppl;
   const int64_t nslots = nb * bs;
@@ -551,21 +631,10 @@ int run_grid(int dtype, const void* xyz, int64_t batch, int64_t cloud_stride, in
       prm.trace_iters = it;
     }
   }
-  {
-    std::lock_guard<std::mutex> lk(g_mu);
-    auto key = std::make_pair(dev, pick->fn);
-    if (!g_attr_done.count(key)) {
-      cudaFuncAttributes fa;
-      e = cudaFuncGetAttributes(&fa, pick->fn);
-      if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(pick->fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)(device_info_nolock(dev).smem_optin - fa.sharedSizeBytes));
-      if (e != cudaSuccess) {
-        ffps::scratch_free(scratch, st);
-        return cuda_fail(e, "cudaFuncSetAttribute(grid)");
-      }
-      g_attr_done[key] = true;
-    }
+  e = prepare_grid_fn(dev, pick->fn);
+  if (e != cudaSuccess) {
+    ffps::scratch_free(scratch, st);
+    return cuda_fail(e, "cudaFuncSetAttribute(grid)");
   }
   void* args[] = {&prm};
   {
@@ -839,7 +908,9 @@ int ffps_auto_schedule_ex(int64_t n, int64_t batch, int dtype) {
     cudaGetLastError();
     return a;
   }
-  return FFPS_ALGO_GRID_CL(grid_cluster(a, batch, device_info(dev).sms, n));
+  int cl = 0;
+  choose_grid(dtype, n, batch, a, dev, &cl);
+  return FFPS_ALGO_GRID_CL(cl);
 }
 
 int ffps_auto_schedule(int64_t n, int64_t batch) {
@@ -918,7 +989,8 @@ int run_kernel_impl(int dtype, const void* xyz, int64_t batch, int64_t cloud_str
     return fail(FFPS_EINVAL, "dtype must be FFPS_F32, FFPS_F64 or FFPS_F32_F64");
   if (algo != FFPS_ALGO_AUTO && algo != FFPS_ALGO_STREAM && algo != FFPS_ALGO_BUCKET &&
       algo != FFPS_ALGO_MULTI && algo != FFPS_ALGO_GRID && algo != FFPS_ALGO_GRID_CL(1) &&
-      algo != FFPS_ALGO_GRID_CL(2) && algo != FFPS_ALGO_GRID_CL(4) && algo != FFPS_ALGO_SMALL)
+      algo != FFPS_ALGO_GRID_CL(2) && algo != FFPS_ALGO_GRID_CL(4) &&
+      algo != FFPS_ALGO_SMALL)
     return fail(FFPS_EINVAL, "unknown algorithm %d", algo);
   if (batch < 0) return fail(FFPS_EINVAL, "batch=%lld < 0", (long long)batch);
   if (batch == 0) return FFPS_OK;

@@ -65,8 +65,8 @@ def test_mixed_random_batches_vs_binary64_oracle(cuda, kind, schedule):
         _check_mixed(_cloud(rng, B, N, kind, np.float32), m, seeds)
 
 
-@pytest.mark.parametrize("sched", ["grid@1", "grid@2", "grid@4", "grid@1/km8", "grid@2/km8",
-                                   "grid@4/km8"])
+@pytest.mark.parametrize("sched", ["grid@1", "grid@2", "grid@4", "grid@1/km8",
+                                   "grid@2/km8", "grid@4/km8"])
 def test_mixed_grid_sizes_ties_and_restricted(cuda, sched):
     """K1g's float-coordinate instances on every bucket size class (32/64/128
     points per bucket), massive ties, candidate prefixes and restricted runs."""

@@ -282,11 +282,12 @@ def test_errors_raised_before_device_work(cuda):
 def test_auto_schedule_choices(cuda):
     """AUTO's measured thresholds (abi.cu auto_algo / grid_cluster) on the
     B200's SM count: 4 CTAs per cloud for >= 40K-point clouds while the
-    batch fits 4 per SM, else 2, else 1; small / stream / bucket below."""
+    batch's 4-CTA clusters are all resident (32 are), else 2 while batch * 2
+    <= SMs, else 1; small / stream / bucket below."""
     sms = torch.cuda.get_device_properties(0).multi_processor_count
     F32, F64, MIX = _native.F32, _native.F64, _native.F32_F64
     for dt in (F32, F64, MIX):
-        assert _native.auto_schedule(50_000, sms // 4, dt) == "grid@4"
+        assert _native.auto_schedule(50_000, 32, dt) == "grid@4"
         assert _native.auto_schedule(50_000, sms // 4 + 1, dt) == "grid@2"
         assert _native.auto_schedule(40_000, 8, dt) == "grid@4"
         assert _native.auto_schedule(39_999, 8, dt) == "grid@2"
@@ -325,7 +326,8 @@ def test_bucketed_schedule_sizes_and_ties(cuda, dtype, sched):
 
 
 @pytest.mark.parametrize("dtype", [np.float32, np.float64])
-@pytest.mark.parametrize("sched", ["grid@1", "grid@2", "grid@4", "grid@2/km8", "grid@4/km8"])
+@pytest.mark.parametrize("sched", ["grid@1", "grid@2", "grid@4", "grid@2/km8",
+                                   "grid@4/km8"])
 def test_multi_winner_degenerate_ties(cuda, dtype, sched):
     """K1g when hundreds of bucket keys tie (identical points, exhausted
     buckets): the candidate list overflows and rounds fall back to one exact
