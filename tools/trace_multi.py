@@ -82,6 +82,21 @@ def main():
                     prev = np.where(ok, d[:, i], prev)
             out.append(f"tail {np.median(t[0, sl, 4] - prev):.0f}")
             print("   D (warp 0, median cycles from the previous mark): " + ", ".join(out))
+    if a.sched.startswith("grid"):
+        # where the loop's cycles go: round 0 (the seed's full scan), the early
+        # rounds, the rest; general-path rounds (warp 0's ncand bit 16)
+        tot = (t[0, :, 4] - t[0, :, 0]).astype(np.float64)
+        gen = ((t[0, :, 6] >> 48) & 1).astype(bool)
+        print(f"loop cycles (CTA 0, rank 0): total {tot.sum():.0f}, mean {tot.mean():.0f} per round")
+        for lo, hi in [(0, 1), (1, 10), (10, R // 10), (R // 10, R)]:
+            if hi <= lo:
+                continue
+            seg = tot[lo:hi]
+            print(f"   rounds [{lo},{hi}): {seg.sum() / tot.sum():6.1%} of the cycles, mean "
+                  f"{seg.mean():.0f}, winners {nsel[lo:hi].sum()}")
+        if gen.any():
+            print(f"   general-path rounds: {gen.sum()} ({tot[gen].sum() / tot.sum():.1%} of the "
+                  f"cycles, mean {tot[gen].mean():.0f})")
 
 
 if __name__ == "__main__":
