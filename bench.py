@@ -617,20 +617,27 @@ def latency_roofline(args, x, budgets, cfg_flash, prec, kern, clocks, B) -> dict
     cycles = float(st[:, 1].mean())
     flagged = float(st[:, 2].mean())
     general = float(st[:, 3].mean()) / max(1, int(sched.split("@")[1]) if "@" in sched else 1)
-    # floor: the same kernel instance (KM = 16, CL, 32-point buckets) on the
+    # floor: the same kernel instance (KM = 16, CL, bucket size) on the
     # smallest table that keeps the standard ranking path: KM bucket groups
     # of 32 buckets per CTA (fewer groups than KM make every round take the
     # general path), a quarter of the points as iterations (the C5 ratio)
-    cl = int(sched.split("@")[1]) if "@" in sched else 1
-    nf = 32 * 32 * 16 * cl
+    gp = _native.grid_plan(PREC_CODE[prec], c1, B, sched)
+    cl, ppl = gp["cl"], gp["ppl"]
+    nf = min(32 * ppl * 32 * 16 * cl, x.shape[1])
     floor_x = x[:, :nf].contiguous()
     prev = _device.set_schedule(sched)
+    prev_ppl = os.environ.get("FFPS_GRID_PPL")
+    os.environ["FFPS_GRID_PPL"] = str(ppl)  # the headline's bucket size class
     try:
         with _device.grid_stats() as gf:
             ffps.fps_batch(floor_x, nf // 4, precision=prec)
             torch.cuda.synchronize()
     finally:
         _device.set_schedule(prev)
+        if prev_ppl is None:
+            os.environ.pop("FFPS_GRID_PPL", None)
+        else:
+            os.environ["FFPS_GRID_PPL"] = prev_ppl
     sf = gf.records[0][3].double()
     f_rounds = float(sf[:, 0].mean())
     f_cycles = float(sf[:, 1].mean())
@@ -647,7 +654,8 @@ def latency_roofline(args, x, budgets, cfg_flash, prec, kern, clocks, B) -> dict
             "rounds_per_cloud": rounds, "winners_per_round": (k1 - 1) / max(rounds, 1.0),
             "cycles_per_round": cpr, "floor_cycles_per_round": floor_cpr,
             "frac_cycles": floor_cpr / cpr,
-            "floor": f"same kernel, {nf}-point clouds (16 bucket groups per CTA), "
+            "floor": f"same kernel ({32 * ppl}-point buckets), {nf}-point clouds (16 bucket "
+                     f"groups per CTA), "
                      f"{nf // 4} iterations, {B} clouds: {f_rounds:.0f} rounds, "
                      f"{f_general:.0f} through the general ranking path",
             "general_path_rounds_per_cloud": general,

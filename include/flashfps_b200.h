@@ -153,6 +153,12 @@ int ffps_auto_schedule(int64_t n, int64_t batch);  /* binary32 arithmetic */
  * schedule from 4,609 points on, binary32 from 10,000). */
 int ffps_auto_schedule_ex(int64_t n, int64_t batch, int dtype);
 
+/* The multi-winner (K1g) configuration for a batch, under FFPS_ALGO_AUTO or a
+ * FFPS_ALGO_GRID_CL(c) schedule: out[0]=CTAs per cloud, out[1]=points per
+ * lane (buckets of 32 x out[1] points), out[2]=buckets per cloud,
+ * out[3]=dynamic shared memory per CTA (bytes). */
+int ffps_grid_plan(int dtype, int64_t n, int64_t batch, int algo, int64_t* out);
+
 /* ffps_run_kernel with an explicit schedule (same arguments; algo as above). */
 int ffps_run_kernel_ex(int dtype, const void* xyz, int64_t batch,
                        int64_t cloud_stride, int64_t n, int64_t iters,

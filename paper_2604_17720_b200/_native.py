@@ -55,6 +55,7 @@ SIGNATURES = {
     "ffps_bucket_plan": (_int, [_int, _i64, ctypes.POINTER(_i64)]),
     "ffps_auto_schedule": (_int, [_i64, _i64]),
     "ffps_auto_schedule_ex": (_int, [_i64, _i64, _int]),
+    "ffps_grid_plan": (_int, [_int, _i64, _i64, _int, ctypes.POINTER(_i64)]),
     "ffps_h2d_prefix": (_int, [_vp, _vp, _i64, _i64, _i64, _int, _vp]),
     "ffps_d2h_prefix": (_int, [_vp, _i64, _vp, _i64, _i64, _i64, _i64, _vp]),
     "ffps_last_launch_count": (_i64, []),
@@ -182,6 +183,15 @@ def auto_schedule(n: int, batch: int, dtype: int = F32) -> str:
     arithmetic of ``dtype`` (F32, F64 or F32_F64)."""
     names = {v: k for k, v in ALGO.items()}
     return names[int(load().ffps_auto_schedule_ex(n, batch, dtype))]
+
+
+def grid_plan(dtype: int, n: int, batch: int, sched: str = "auto") -> dict:
+    """K1g configuration for a batch under ``sched`` ("auto" or "grid@c"):
+    CTAs per cloud, points per lane (bucket = 32 x ppl points), buckets per
+    cloud, dynamic shared memory per CTA."""
+    out = (ctypes.c_int64 * 4)()
+    check(load().ffps_grid_plan(dtype, n, batch, ALGO[sched], out), "ffps_grid_plan")
+    return dict(zip(("cl", "ppl", "buckets", "smem"), (int(v) for v in out)))
 
 
 def h2d_prefix(dst, src_host, batch, n_prefix, cloud_stride, dtype, stream) -> None:

@@ -450,12 +450,26 @@ struct GridPick {
   size_t smem = 0;  // dynamic shared memory per CTA
 };
 
-// the smallest bucket size whose per-rank table fits shared memory
+// Bucket size class (32 x PPL points): the smallest whose per-rank table
+// holds at most kGridBucketsPerCta buckets and fits shared memory (else the
+// smallest that fits).  Measured over 25K-150K candidates, 16 and 64 clouds,
+// 1/2/4 CTAs per cloud, binary64 (profiles/r02_sweep_ppl_f64.txt,
+// tools/gpu_ppl.sh): the fastest class had 390-600 buckets per CTA (782:
+// within 2%) — larger tables pay in the group statistics and ranking, more
+// buckets per point in the flag phase (50K candidates on 2 CTAs: 782 buckets
+// of 32 points per CTA 7.82 ms, 391 of 64 points 7.63 ms; 150K: 586 of 128
+// points 24.7 ms, 2,344 of 32 points 30.7 ms).  FFPS_GRID_PPL (A/B) sets the
+// smallest class.
+constexpr int64_t kGridBucketsPerCta = 700;
+
 GridPick pick_grid(int dtype, int64_t n, int cl, int km, const DeviceInfo& di) {
   int cnt = 0;
   const ffps::GridInst* insts = ffps::grid_instances(&cnt);
-  GridPick g;
-  for (int ppl = 1; ppl <= 8 && !g.inst; ppl *= 2) {
+  int ppl0 = 1;
+  if (const char* v = getenv("FFPS_GRID_PPL")) ppl0 = std::max(1, std::min(8, atoi(v)));
+  GridPick best;
+  for (int ppl = ppl0; ppl <= 8; ppl *= 2) {
+    GridPick g;
     g.nb = (n + 32 * ppl - 1) / (32 * ppl);
     const int64_t nbl = (g.nb + cl - 1) / cl;  // buckets of cluster rank 0 (the most)
     if (nbl > 4096) continue;                  // <= 128 bucket groups per CTA
@@ -470,8 +484,14 @@ GridPick pick_grid(int dtype, int64_t n, int cl, int km, const DeviceInfo& di) {
         }
         if (g.smem + fa.sharedSizeBytes <= di.smem_optin) g.inst = &insts[i];  // + static smem
       }
+    if (!g.inst) continue;
+    if (!best.inst) best = g;          // the smallest class that fits
+    if (nbl <= kGridBucketsPerCta) {   // the smallest with a table of the measured size
+      best = g;
+      break;
+    }
   }
-  return g;
+  return best;
 }
 
 cudaError_t prepare_grid_fn(int dev, const void* fn) {
@@ -911,6 +931,26 @@ int ffps_auto_schedule_ex(int64_t n, int64_t batch, int dtype) {
   int cl = 0;
   choose_grid(dtype, n, batch, a, dev, &cl);
   return FFPS_ALGO_GRID_CL(cl);
+}
+
+int ffps_grid_plan(int dtype, int64_t n, int64_t batch, int algo, int64_t* out) {
+  if ((dtype != FFPS_F32 && dtype != FFPS_F64 && dtype != FFPS_F32_F64) || n < 1 || batch < 1 ||
+      !out)
+    return fail(FFPS_EINVAL, "ffps_grid_plan: bad arguments");
+  if (algo == FFPS_ALGO_AUTO) algo = FFPS_ALGO_GRID;
+  if ((algo & 0xff) != FFPS_ALGO_GRID)
+    return fail(FFPS_EINVAL, "ffps_grid_plan: algo must be AUTO or a grid schedule");
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+  int cl = 0;
+  const GridPick g = choose_grid(dtype, n, batch, algo, dev, &cl);
+  if (!g.inst) return fail(FFPS_EUNSUPPORTED, "no grid configuration for n=%lld", (long long)n);
+  out[0] = cl;
+  out[1] = g.inst->ppl;
+  out[2] = g.nb;
+  out[3] = (int64_t)g.smem;
+  return FFPS_OK;
 }
 
 int ffps_auto_schedule(int64_t n, int64_t batch) {

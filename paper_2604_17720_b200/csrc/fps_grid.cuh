@@ -248,13 +248,11 @@ __global__ void __launch_bounds__(NT, 1) fps_grid_kernel(const BucketParams prm)
   int32_t* rlist = reinterpret_cast<int32_t*>(pmask + nb);  // [nb] round list
   uint32_t* cand_p = reinterpret_cast<uint32_t*>(rlist + nb);  // [NCG ng]
   int32_t* cand_q = reinterpret_cast<int32_t*>(cand_p + NCG * ng);  // [NCG ng]
-  int32_t* gdirty = cand_q + NCG * ng;  // [ng] group has a re-evaluated bucket this round
   // FFPS_F32_F64: the flag phase tests in binary32, rounded down, against the
   // keys rounded up (box_lb_rd): shadow keys of the buckets and group maxima
   constexpr bool SHADOW = sizeof(T) == 8 && sizeof(S) == 4;
-  float* kv32 = reinterpret_cast<float*>(gdirty + ng + ng);  // [nb] (after dlist)
+  float* kv32 = reinterpret_cast<float*>(cand_q + NCG * ng);  // [nb]
   float* gmax32 = kv32 + nb;                                 // [ng]
-  int32_t* dlist = gdirty + ng;       // [ng] dirty groups
   // phase D: per-warp candidate list (<= 32)
   __shared__ bits_t cv_w[1][64];
   __shared__ uint32_t ci_w[1][64];
@@ -363,7 +361,6 @@ __global__ void __launch_bounds__(NT, 1) fps_grid_kernel(const BucketParams prm)
     }
     gmax[g] = A::bits(A::pinf());
     if constexpr (SHADOW) gmax32[g] = __int_as_float(0x7f800000);
-    gdirty[g] = 0;
   }
   __syncthreads();
   const T full_r2 = (T)(kFullFrac * kFullFrac * (double)ext_s * (double)ext_s);
