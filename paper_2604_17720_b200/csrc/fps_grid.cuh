@@ -637,7 +637,10 @@ __global__ void __launch_bounds__(NT, 1) fps_grid_kernel(const BucketParams prm)
 #ifndef FFPS_GRID_CH1
 #define FFPS_GRID_CH1 4
 #endif
-      constexpr int CH = PPL <= 1 ? FFPS_GRID_CH1 : (PPL == 2 ? 2 : 1);  // <= 4 points per lane in flight
+#ifndef FFPS_GRID_CH2
+#define FFPS_GRID_CH2 2
+#endif
+      constexpr int CH = PPL <= 1 ? FFPS_GRID_CH1 : (PPL == 2 ? FFPS_GRID_CH2 : 1);  // buckets in flight
       for (int e = warp; e < nr; e += CH * NW) {
         const int nv = (nr - e + NW - 1) / NW;
         if (nv >= CH) batch(std::integral_constant<int, CH>{}, e);
