@@ -649,7 +649,7 @@ def latency_roofline(args, x, budgets, cfg_flash, prec, kern, clocks, B) -> dict
     achieved = rounds / (kms / 1e3)                  # rounds/s per cloud, event-timed
     return {"bound": "latency", "achieved": achieved, "peak": peak,
             "unit": "greedy rounds/s per cloud", "frac": achieved / peak,
-            "traffic": dram_traffic("fps_grid_kernel", prec),
+            "traffic": dram_traffic("fps_grid_kernel", prec, f"512, {ppl}, 16, {cl}>"),
             "kernel": "fps_grid_kernel (K1g) " + sched, "kernel_ms": kms,
             "rounds_per_cloud": rounds, "winners_per_round": (k1 - 1) / max(rounds, 1.0),
             "cycles_per_round": cpr, "floor_cycles_per_round": floor_cpr,
@@ -668,16 +668,18 @@ def latency_roofline(args, x, budgets, cfg_flash, prec, kern, clocks, B) -> dict
                 "gbs": units * BYTES_PER_UNIT[prec] / (kms / 1e3) / 1e9}}
 
 
-def dram_traffic(kname: str, prec: str = "f64"):
+def dram_traffic(kname: str, prec: str = "f64", inst: str = ""):
     """Per-launch DRAM bytes of a kernel from one `ncu --set full` capture
-    (profiles/traffic.json), or None: the instance of the headline's
-    arithmetic (float coordinates + binary64 = <double, float, ...>) first."""
+    (profiles/traffic.json), or None: the exact template instance when given
+    (e.g. "512, 2, 16, 2>"), else the instance of the headline's arithmetic
+    (float coordinates + binary64 = <double, float, ...>)."""
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
             tj = json.load(fh)
         tag = "<double, float," if prec == "f64" else "<float,"
-        hit = [v for k_, v in tj.items() if kname in k_ and tag in k_] or \
-              [v for k_, v in tj.items() if kname in k_]
+        hit = [v for k_, v in tj.items() if kname in k_ and tag in k_ and inst in k_]
+        if not inst:
+            hit = hit or [v for k_, v in tj.items() if kname in k_]
         return hit[0]["dram_bytes"] if hit else None
     except (OSError, ValueError, KeyError):
         return None
