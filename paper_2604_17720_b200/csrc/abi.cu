@@ -453,20 +453,23 @@ struct GridPick {
 // Bucket size class (32 x PPL points): the smallest whose per-rank table
 // holds at most kGridBucketsPerCta buckets and fits shared memory (else the
 // smallest that fits).  Measured over 25K-150K candidates, 16 and 64 clouds,
-// 1/2/4 CTAs per cloud, binary64 (profiles/r02_sweep_ppl_f64.txt,
-// tools/gpu_ppl.sh): the fastest class had 390-600 buckets per CTA (782:
-// within 2%) — larger tables pay in the group statistics and ranking, more
-// buckets per point in the flag phase (50K candidates on 2 CTAs: 782 buckets
-// of 32 points per CTA 7.82 ms, 391 of 64 points 7.63 ms; 150K: 586 of 128
-// points 24.7 ms, 2,344 of 32 points 30.7 ms).  FFPS_GRID_PPL (A/B) sets the
-// smallest class.
-constexpr int64_t kGridBucketsPerCta = 700;
+// 1/2/4 CTAs per cloud, binary64, uniform and LiDAR-like clouds
+// (profiles/r02_sweep_ppl_f64.txt, r02_ab_ppl_uniform_lidar.txt,
+// tools/gpu_ppl*.sh): tables of ~1,200+ buckets per CTA pay in the group
+// statistics and ranking (75K candidates on 2 CTAs: 1,172 buckets of 32 points
+// per CTA 13.2 ms, 586 of 64 points 11.5 ms uniform / 13.2 vs 12.2 LiDAR;
+// 150K: 586 of 128 points 24.7 ms, 2,344 of 32 points 30.7 ms), while tables of
+// fewer than 16 groups take the general ranking path often on uneven clouds
+// (50K on 2 CTAs: 782 buckets of 32 points 7.78 ms uniform / 7.96 LiDAR, 391
+// of 64 points 7.64 / 8.65).  FFPS_GRID_PPL (A/B) sets the class.
+constexpr int64_t kGridBucketsPerCta = 800;
 
 GridPick pick_grid(int dtype, int64_t n, int cl, int km, const DeviceInfo& di) {
   int cnt = 0;
   const ffps::GridInst* insts = ffps::grid_instances(&cnt);
-  int ppl0 = 1;
+  int ppl0 = 1;  // FFPS_GRID_PPL (A/B): this bucket size class when it fits
   if (const char* v = getenv("FFPS_GRID_PPL")) ppl0 = std::max(1, std::min(8, atoi(v)));
+  const bool exact = getenv("FFPS_GRID_PPL") != nullptr;
   GridPick best;
   for (int ppl = ppl0; ppl <= 8; ppl *= 2) {
     GridPick g;
@@ -486,7 +489,7 @@ GridPick pick_grid(int dtype, int64_t n, int cl, int km, const DeviceInfo& di) {
       }
     if (!g.inst) continue;
     if (!best.inst) best = g;          // the smallest class that fits
-    if (nbl <= kGridBucketsPerCta) {   // the smallest with a table of the measured size
+    if (exact || nbl <= kGridBucketsPerCta) {  // the smallest with a table of the measured size
       best = g;
       break;
     }

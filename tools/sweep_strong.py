@@ -44,10 +44,19 @@ def main():
     ap.add_argument("--iters", type=int, default=12_500)
     ap.add_argument("--scheds", nargs="*", default=["grid@1", "grid@2", "grid@4", "grid@2/km8"])
     ap.add_argument("--precisions", nargs="*", default=["f64", "f32"])
+    ap.add_argument("--cloud", choices=["uniform", "lidar"], default="uniform")
+    ap.add_argument("--cloud-n", type=int, default=0,
+                    help="LiDAR frame size (the candidates are its first n points); 0: 4 n")
     a = ap.parse_args()
-    g = torch.Generator(device="cuda").manual_seed(0)
-    x = torch.rand((max(a.batches), a.n, 3), generator=g, device="cuda",
-                   dtype=torch.float64).float()
+    if a.cloud == "lidar":
+        sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+        import bench
+        frames = bench.make_clouds("lidar", max(a.batches), a.cloud_n or 4 * a.n, 0)
+        x = torch.from_numpy(np.ascontiguousarray(frames[:, :a.n])).cuda()
+    else:
+        g = torch.Generator(device="cuda").manual_seed(0)
+        x = torch.rand((max(a.batches), a.n, 3), generator=g, device="cuda",
+                       dtype=torch.float64).float()
     for B in a.batches:
         xb = x[:B].contiguous()
         for prec in a.precisions:
