@@ -95,8 +95,12 @@ def main():
             print(f"   rounds [{lo},{hi}): {seg.sum() / tot.sum():6.1%} of the cycles, mean "
                   f"{seg.mean():.0f}, winners {nsel[lo:hi].sum()}")
         if gen.any():
+            nct = (t[0, :, 6] >> 32) & 0xffff
+            ng_ = nct[gen]
             print(f"   general-path rounds: {gen.sum()} ({tot[gen].sum() / tot.sum():.1%} of the "
-                  f"cycles, mean {tot[gen].mean():.0f})")
+                  f"cycles, mean {tot[gen].mean():.0f}); keys >= tau2: <= 32 {(ng_ <= 32).sum()}, "
+                  f"33-64 {((ng_ > 32) & (ng_ <= 64)).sum()}, > 64 (one winner) {(ng_ > 64).sum()}; "
+                  f"winners/round {nsel[gen].mean():.2f} vs {nsel[~gen].mean():.2f}")
 
 
 if __name__ == "__main__":
