@@ -50,6 +50,8 @@ def test_abi_version_and_argument_errors_without_gpu():
     assert lib.ffps_run_kernel(0, None, 0, 10, 10, 5, None, None, 0, None, None, 5, None) == 0
     out = (ctypes.c_int64 * 7)()
     assert lib.ffps_plan(0, 0, 1, out) == -1
+    assert lib.ffps_grid_plan(7, 1000, 1, 0, out) == -1    # bad dtype, before any CUDA call
+    assert lib.ffps_grid_plan(0, 0, 1, 0, out) == -1
 
 
 def test_reference_errors_precede_device_requirement():

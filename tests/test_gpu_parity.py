@@ -299,6 +299,25 @@ def test_auto_schedule_choices(cuda):
     assert _native.auto_schedule(9_000, 64, F32) == "bucket"
 
 
+def test_grid_plan_bucket_size_rule(cuda):
+    """K1g's bucket size class (abi.cu pick_grid): the smallest class whose
+    per-CTA table holds at most 800 buckets, under AUTO's cluster choice."""
+    F64 = _native.F32_F64
+    p = _native.grid_plan(F64, 50_000, 64)           # C5 headline: 2 CTAs, 782 buckets / CTA
+    assert (p["cl"], p["ppl"], p["buckets"]) == (2, 1, 1563)
+    p = _native.grid_plan(F64, 75_000, 64)           # 1,172 -> 586 buckets of 64 points / CTA
+    assert (p["cl"], p["ppl"]) == (2, 2)
+    p = _native.grid_plan(F64, 150_000, 64)
+    assert (p["cl"], p["ppl"]) == (2, 4)
+    p = _native.grid_plan(F64, 75_000, 16)           # 4 CTAs: 586 buckets of 32 points / CTA
+    assert (p["cl"], p["ppl"]) == (4, 1)
+    p = _native.grid_plan(F64, 50_000, 8, "grid@1")
+    assert p["cl"] == 1 and (p["buckets"] + p["cl"] - 1) // p["cl"] <= 800
+    assert p["smem"] > 0
+    with pytest.raises(ffps.errors.KernelError):
+        _native.grid_plan(F64, 50_000, 8, "stream")
+
+
 def test_abi_rejects_bad_arguments(cuda):
     lib = _native.load()
     rc = lib.ffps_run_kernel(0, 1, 1, 10, 10, 11, 1, None, 0, 1, 1, 11, None)
